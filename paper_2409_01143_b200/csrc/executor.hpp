@@ -1,0 +1,42 @@
+// Per-rank executor of one asymmetric-parallel training step.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "plan.hpp"
+
+namespace hexexec {
+
+struct ExecConfig {
+  uint64_t seed = 0;
+  float lr = 1e-3f, beta1 = 0.9f, beta2 = 0.95f, eps = 1e-8f, weight_decay = 0.1f;
+  std::string sm_cap = "green";       // "green" | "cta" | "none"
+  std::string dp_comm_dtype = "bf16"; // "bf16" | "fp32"
+  bool validate_only = false;
+};
+
+ExecConfig parse_exec_config(const std::string& text);
+
+class Executor;
+
+Executor* make_executor(const std::string& cluster, const std::string& model,
+                                        const std::string& plan, const std::string& cfg,
+                                        int world_rank, int world_size, int cuda_device,
+                                        const void* uid, size_t uid_len);
+void executor_step(Executor& e, const int32_t* tokens_host, size_t n, float* loss_out);
+void executor_step_async(Executor& e);
+void executor_sync(Executor& e);
+float executor_last_loss(Executor& e);
+void executor_synth_tokens(const Executor& e, int64_t step, int32_t* out, size_t n);
+bool executor_tensor_info(const Executor& e, const std::string& name, int64_t* row0,
+                          int64_t* rows, int64_t* cols, int64_t* grows);
+void executor_read_tensor(Executor& e, const std::string& name, int which, float* out,
+                          size_t n);
+std::string executor_stats_json(const Executor& e);
+void destroy_executor(Executor* e);
+
+}  // namespace hexexec

@@ -1,0 +1,53 @@
+// Host-side interface of the sm_100a tcgen05 GEMM used for every dense
+// contraction of the step (TP column/row GEMMs fwd + dgrad + wgrad, LM head,
+// attention score / context products).
+//
+//   C[z][m, n] = alpha * sum_k A[z][m, k] * B[z][n, k]   (+ C[z][m, n] if beta)
+//
+// A is logically [M, K], B logically [N, K].  Each is stored either K-major
+// (K contiguous, row stride ld) or MN-major (M resp. N contiguous, stride ld
+// between consecutive k).  Batch index z = z1 + nb1 * z2 with element strides
+// bs1 / bs2, so per-head attention products address the fused QKV buffer in
+// place.  Inputs bf16; accumulation fp32 in TMEM; C bf16 or fp32.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hexexec {
+
+struct GemmOperand {
+  const void* ptr = nullptr;
+  int mn_major = 0;
+  long long ld = 0;   // elements between consecutive rows (K-major) / k (MN-major)
+  long long bs1 = 0;  // batch strides in elements
+  long long bs2 = 0;
+};
+
+enum GemmCausal : int {
+  kCausalNone = 0,
+  kCausalSkipUpper = 1,  // tiles with n0 > m0 + BM - 1 are not computed (nor written)
+  kCausalKLower = 2,     // k range limited to [0, min(K, m0 + BM))   (A lower-triangular)
+  kCausalKUpper = 3,     // k range limited to [m0, K)                  (A^T of lower-tri)
+};
+
+struct GemmDesc {
+  int M = 0, N = 0, K = 0;
+  int nb1 = 1, nb2 = 1;
+  GemmOperand A, B;
+  void* C = nullptr;
+  long long ldc = 0, cbs1 = 0, cbs2 = 0;
+  int c_fp32 = 0;  // 1: fp32 output, 0: bf16 output
+  int beta = 0;    // 1: C += alpha*acc (fp32 C only)
+  float alpha = 1.f;
+  int causal = kCausalNone;
+};
+
+// Launch on `stream`.  Returns cudaSuccess or the launch error.  Tensor maps
+// are encoded on the host per call (cheap, ~1 us) from the descriptor.
+cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream);
+
+// number of SMs the GEMM may occupy (0 = all); used for SM-capped ranks
+void gemm_set_sm_limit(int sms);
+
+}  // namespace hexexec
