@@ -1,0 +1,158 @@
+"""Writes the cluster / model / plan documents of the BASELINE configs.
+
+Cluster and model documents follow the reference formats
+(/root/reference/proj/src/json_io.cpp:80-191) plus extension keys the
+reference parser ignores.  Planner plans (cfg3, cfg5, even-split baselines)
+are produced by the reference scheduler itself (oracle/_ref, built by
+oracle/Makefile) and committed, so nothing here runs on the GPU box.
+
+    python configs/make_configs.py          # needs oracle/_ref/libhexplan_ref.so
+"""
+import json
+import os
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+
+F, HALF, THIRD = 2250.0, 1125.0, 750.0
+
+
+def cluster(devs, machines=None):
+    machines = machines or {"box": [d for d, _ in devs]}
+    mdoc = {m: {"intra_bandwidth_gbps": 900, "intra_latency_us": 3} for m in machines}
+    where = {d: m for m, ds in machines.items() for d in ds}
+    return {"machines": mdoc,
+            "devices": [{"id": d, "machine": where[d], "memory_gib": 178, "peak_tflops": p}
+                        for d, p in devs],
+            "inter": {"bandwidth_gbps": 900, "latency_us": 3}}
+
+
+TIERS8 = [("g0", F), ("g1", F), ("g2", F), ("g3", F), ("g4", HALF), ("g5", HALF),
+          ("g6", THIRD), ("g7", THIRD)]
+CLUSTERS = {
+    "b200_1": cluster([("g0", F)]),
+    "b200_2_capped": cluster([("g0", F), ("g1", THIRD)]),
+    "b200_2_even": cluster([("g0", F), ("g1", F)]),
+    "b200_4_tiers": cluster([("g0", F), ("g1", F), ("g2", HALF), ("g3", HALF)]),
+    "b200_4_even": cluster([("g0", F), ("g1", F), ("g2", F), ("g3", F)]),
+    "b200_8_onebox": cluster(TIERS8),
+    "b200_8_tiers": cluster(TIERS8, {"tierF": ["g0", "g1", "g2", "g3"], "tierH": ["g4", "g5"],
+                                     "tierT": ["g6", "g7"]}),
+    "b200_8_even": cluster([(f"g{i}", F) for i in range(8)]),
+}
+
+MODELS = {
+    "tiny": {"num_layers": 4, "hidden_dim": 256, "seq_len": 128, "bytes_per_element": 4,
+             "num_heads": 4, "ffn_dim": 1024, "vocab_size": 512},
+    "llama7b_4l": {"num_layers": 4, "hidden_dim": 4096, "seq_len": 2048, "bytes_per_element": 2,
+                   "num_heads": 32, "ffn_dim": 11008, "vocab_size": 32000},
+    "llama7b": {"num_layers": 32, "hidden_dim": 4096, "seq_len": 2048, "bytes_per_element": 2,
+                "num_heads": 32, "ffn_dim": 11008, "vocab_size": 32000},
+    "llama13b": {"num_layers": 40, "hidden_dim": 5120, "seq_len": 2048, "bytes_per_element": 2,
+                 "num_heads": 40, "ffn_dim": 13824, "vocab_size": 32000},
+    "llama30b": {"num_layers": 60, "hidden_dim": 6656, "seq_len": 2048, "bytes_per_element": 2,
+                 "num_heads": 52, "ffn_dim": 17920, "vocab_size": 32000},
+}
+
+
+def stage(devs, start, count, widths=None):
+    s = {"devices": devs, "tp": len(devs), "layer_start": start, "layer_count": count}
+    if widths:
+        s["tp_widths"] = widths
+    return s
+
+
+def pipe(batch, mb, stages):
+    return {"batch": batch, "micro_batch": mb, "num_micro_batches": batch // mb,
+            "stages": stages}
+
+
+def plan(pipes, L):
+    gb = sum(p["batch"] for p in pipes)
+    groups = [{"layer": l, "members": []} for l in range(L)]
+    for p in pipes:
+        for s in p["stages"]:
+            for l in range(s["layer_start"], s["layer_start"] + s["layer_count"]):
+                groups[l]["members"].append(s["devices"][0])
+    return {"global_batch": gb, "pipelines": pipes, "dp_groups": groups}
+
+
+HAND = {
+    # cfg1: tiny GPT, 2-rank asymmetric plans (TP widths 3:1; DP micro-batches 5:3)
+    "tiny_1": ("b200_1", "tiny", plan([pipe(8, 4, [stage(["g0"], 0, 4)])], 4)),
+    "tiny_tp31": ("b200_2_capped", "tiny", plan([pipe(8, 4, [stage(["g0", "g1"], 0, 4, [3, 1])])], 4)),
+    "tiny_dp53": ("b200_2_capped", "tiny", plan([pipe(5, 1, [stage(["g0"], 0, 4)]),
+                                                 pipe(3, 1, [stage(["g1"], 0, 4)])], 4)),
+    "tiny_pp31": ("b200_2_capped", "tiny", plan([pipe(8, 2, [stage(["g0"], 0, 3),
+                                                             stage(["g1"], 3, 1)])], 4)),
+    "tiny_mixed4": ("b200_4_tiers", "tiny", plan([
+        pipe(5, 1, [stage(["g0", "g2"], 0, 3, [2, 1]), stage(["g3"], 3, 1)]),
+        pipe(3, 1, [stage(["g1"], 0, 4)])], 4)),
+    # N=1 workload: the cfg2 model on one B200
+    "llama7b_4l_1gpu": ("b200_1", "llama7b_4l", plan([pipe(8, 1, [stage(["g0"], 0, 4)])], 4)),
+    # cfg2: Llama-7B 4-layer block, TP=2 with 3:1 widths, rank 1 capped to 1/3 SMs
+    "llama7b_4l_tp31": ("b200_2_capped", "llama7b_4l",
+                        plan([pipe(8, 1, [stage(["g0", "g1"], 0, 4, [3, 1])])], 4)),
+    "llama7b_4l_tp11_even": ("b200_2_even", "llama7b_4l",
+                             plan([pipe(8, 1, [stage(["g0", "g1"], 0, 4)])], 4)),
+    # cfg4: Llama-13B, 3 stages 16/14/10, asymmetric TP inside stages
+    "llama13b_pp3_asymtp": ("b200_8_onebox", "llama13b", plan([pipe(16, 1, [
+        stage(["g0", "g1", "g4"], 0, 16, [2, 2, 1]),
+        stage(["g2", "g3", "g5"], 16, 14, [2, 2, 1]),
+        stage(["g6", "g7"], 30, 10)])], 40)),
+}
+
+PLANNED = {
+    # cfg3: Llama-7B on 8 B200 tiers; asymmetric DP with uneven micro-batch counts
+    "llama7b_8_asym": ("b200_8_onebox", "llama7b", "schedule",
+                       {"global_batch": 64, "iterations": 50, "seed": 0, "threads": 8,
+                        "state_multiplier": 2.5}),
+    "llama7b_8_even": ("b200_8_even", "llama7b", "symmetric",
+                       {"global_batch": 64, "iterations": 50, "seed": 0, "threads": 8,
+                        "state_multiplier": 2.5}),
+    # cfg5: Llama-30B layers under a full plan from the hierarchical partitioner
+    "llama30b_8_tiers": ("b200_8_tiers", "llama30b", "schedule",
+                         {"global_batch": 64, "iterations": 50, "seed": 0, "threads": 8,
+                          "state_multiplier": 2.5}),
+    # N=4 scaling point
+    "llama7b_4l_4_asym": ("b200_4_tiers", "llama7b_4l", "schedule",
+                          {"global_batch": 16, "iterations": 30, "seed": 0, "threads": 8,
+                           "state_multiplier": 2.5}),
+    "llama7b_4l_2_asym": ("b200_2_capped", "llama7b_4l", "schedule",
+                          {"global_batch": 8, "iterations": 20, "seed": 0, "threads": 8,
+                           "state_multiplier": 2.5}),
+}
+
+
+def write(path, obj):
+    with open(path, "w") as f:
+        json.dump(obj, f, indent=2)
+        f.write("\n")
+
+
+def main():
+    for sub in ("clusters", "models", "plans"):
+        os.makedirs(os.path.join(HERE, sub), exist_ok=True)
+    for k, v in CLUSTERS.items():
+        write(os.path.join(HERE, "clusters", k + ".json"), v)
+    for k, v in MODELS.items():
+        write(os.path.join(HERE, "models", k + ".json"), v)
+    index = {}
+    for k, (c, m, p) in HAND.items():
+        write(os.path.join(HERE, "plans", k + ".json"), p)
+        index[k] = {"cluster": c, "model": m, "source": "hand"}
+    from oracle import refshim
+    for k, (c, m, kind, cfg) in PLANNED.items():
+        res = refshim.plan(json.dumps(CLUSTERS[c]), json.dumps(MODELS[m]), json.dumps(cfg), kind)
+        assert res["found"], (k, res)
+        with open(os.path.join(HERE, "plans", k + ".json"), "w") as f:
+            f.write(res["plan"])
+        index[k] = {"cluster": c, "model": m, "source": f"hexplan_{kind}", "config": cfg,
+                    "predicted_s": res["cost"], "predicted_mfu": res["mfu"]}
+        print(k, round(res["cost"], 6), round(res["mfu"], 4))
+    write(os.path.join(HERE, "index.json"), index)
+
+
+if __name__ == "__main__":
+    main()

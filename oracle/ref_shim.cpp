@@ -87,7 +87,8 @@ hexplan::ExecutionPlan plan_from_json(const std::string& text,
 
 ojson ids(const std::vector<int>& v, const hexplan::ClusterSpec& c) {
   ojson a = ojson::array();
-  for (int i : v) a.push_back(c.devices[i].id);
+  for (int i : v)
+    a.push_back(i >= 0 && i < int(c.devices.size()) ? ojson(c.devices[i].id) : ojson(i));
   return a;
 }
 
@@ -111,7 +112,14 @@ int hexref_check_plan(const char* cluster_json, const char* model_json,
     r["num_micro_batches"] = ojson::array();
     for (const auto& p : plan.pipelines) r["num_micro_batches"].push_back(p.num_micro_batches());
     hexplan::ExecutionPlan rebuilt = plan;
-    hexplan::build_dp_groups(rebuilt, m);
+    // the reference build_dp_groups reads stage.devices[0] unchecked; skip it for
+    // stage-less-device plans (validate_plan rejects them anyway)
+    bool any_empty = false;
+    for (const auto& p : plan.pipelines)
+      for (const auto& st : p.stages)
+        any_empty |= st.devices.empty() || st.layer_start < 0 ||
+                     st.layer_start + st.layer_count > m.num_layers;
+    if (!any_empty) hexplan::build_dp_groups(rebuilt, m);
     r["dp_groups"] = ojson::array();
     for (const auto& g : rebuilt.dp_groups)
       r["dp_groups"].push_back({{"layer", g.layer}, {"members", ids(g.members, c)}});
@@ -122,7 +130,7 @@ int hexref_check_plan(const char* cluster_json, const char* model_json,
     } catch (const std::exception& e) {
       r["validate"] = e.what();
     }
-    try {
+    if (r["validate"] == "ok") try {
       hexplan::CostReport rep = hexplan::iteration_time(plan, m, c, 1.0);
       r["cost"] = ojson::parse(hexplan::serialize_report(rep, c));
     } catch (const std::exception& e) {

@@ -16,7 +16,7 @@ if not os.path.exists(LIB_PATH):
         f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
         "(there is no CPU fallback)")
 
-lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+lib = C.CDLL(LIB_PATH)
 
 OK, ERR_PARSE, ERR_INVALID, ERR_INFEASIBLE, ERR_LIMIT, ERR_INTERNAL, ERR_CUDA, ERR_NCCL = range(8)
 STATUS_NAMES = {0: "OK", 1: "PARSE", 2: "INVALID", 3: "INFEASIBLE", 4: "LIMIT",

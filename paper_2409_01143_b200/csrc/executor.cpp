@@ -1,0 +1,1118 @@
+// Per-rank executor of one asymmetric-parallel training step.
+//
+// One process per GPU.  The rank's role (pipeline, stage, TP index, shard
+// ranges, samples, PP peers, DP buckets) comes from build_layout (plan.cpp).
+// The step is:
+//   1F1B over the pipeline's micro-batches (Megatron non-interleaved order;
+//   reference prices it as fill + (n-1)*bottleneck, cost_model.cpp:96-111):
+//     fwd per layer: RMSNorm -> QKV GEMM (column shard) -> RoPE -> causal
+//       attention (batched tcgen05 GEMMs + warp softmax) -> O GEMM (row shard)
+//       -> TP allreduce -> RMSNorm -> gate/up GEMM -> SwiGLU -> down GEMM ->
+//       TP allreduce;  last stage: final norm, vocab-parallel LM head + CE.
+//     bwd mirrors it (dgrad + wgrad GEMMs, TP allreduce of input grads).
+//     PP activations / grads move with NCCL send/recv on the world comm.
+//   DP: per-tensor scale by (batch_i / global_batch) / multiplicity fused with
+//     the bf16 cast, then NCCL allreduce per chunk-matched bucket.
+//   AdamW on the fp32 master shard, refreshing the bf16 copy.
+// Every kernel is ours (csrc/*.cu); there is no host compute path.
+#include "executor.hpp"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <sstream>
+
+#include "gemm.h"
+#include "kernels.h"
+#include "nlohmann/json.hpp"
+
+namespace hexexec {
+
+using ojson = nlohmann::ordered_json;
+
+#define HX_CUDA(x)                                                                         \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_) + " (" __FILE__ ":" + \
+                      std::to_string(__LINE__) + ")");                                     \
+  } while (0)
+
+#define HX_NCCL(x)                                                                        \
+  do {                                                                                    \
+    ncclResult_t r_ = (x);                                                                \
+    if (r_ != ncclSuccess)                                                                \
+      throw NcclError(std::string(#x) + ": " + ncclGetErrorString(r_) + " (" __FILE__ ":" + \
+                      std::to_string(__LINE__) + ")");                                    \
+  } while (0)
+
+ExecConfig parse_exec_config(const std::string& text) {
+  ExecConfig c;
+  if (text.empty()) return c;
+  ojson j = ojson::parse(text, nullptr, false);
+  if (j.is_discarded() || !j.is_object()) throw ParseError("exec config: not a JSON object");
+  for (auto& [k, v] : j.items()) {
+    try {
+      if (k == "seed") c.seed = v.get<uint64_t>();
+      else if (k == "lr") c.lr = v.get<float>();
+      else if (k == "beta1") c.beta1 = v.get<float>();
+      else if (k == "beta2") c.beta2 = v.get<float>();
+      else if (k == "eps") c.eps = v.get<float>();
+      else if (k == "weight_decay") c.weight_decay = v.get<float>();
+      else if (k == "sm_cap") c.sm_cap = v.get<std::string>();
+      else if (k == "dp_comm_dtype") c.dp_comm_dtype = v.get<std::string>();
+      else if (k == "validate_only") c.validate_only = v.get<bool>();
+      else throw ParseError("exec config: unknown key '" + k + "'");
+    } catch (const nlohmann::json::exception& e) {
+      throw ParseError("exec config: bad value for '" + k + "'");
+    }
+  }
+  if (c.sm_cap != "green" && c.sm_cap != "cta" && c.sm_cap != "none")
+    throw ParseError("exec config: sm_cap must be green|cta|none");
+  if (c.dp_comm_dtype != "bf16" && c.dp_comm_dtype != "fp32")
+    throw ParseError("exec config: dp_comm_dtype must be bf16|fp32");
+  return c;
+}
+
+namespace {
+
+// bump allocator over one device allocation
+class Arena {
+ public:
+  void reserve(size_t bytes) { total_ += align(bytes); }
+  void commit() {
+    if (total_) HX_CUDA(cudaMalloc(&base_, total_));
+  }
+  template <typename T>
+  T* take(size_t count) {
+    size_t b = align(count * sizeof(T));
+    if (used_ + b > total_) throw std::runtime_error("arena overflow");
+    T* p = reinterpret_cast<T*>(static_cast<char*>(base_) + used_);
+    used_ += b;
+    return p;
+  }
+  void release() {
+    if (base_) cudaFree(base_);
+    base_ = nullptr;
+  }
+  size_t total() const { return total_; }
+
+ private:
+  static size_t align(size_t b) { return (b + 255) / 256 * 256; }
+  void* base_ = nullptr;
+  size_t total_ = 0, used_ = 0;
+};
+
+struct LayerActs {
+  float* x_mid;     // [M, H]
+  bf16* xn;         // [M, H]
+  float* rstd1;     // [M]
+  bf16* qkv;        // [M, 3 d nh]
+  bf16* P;          // [mb * nh, S, S]
+  bf16* attn;       // [M, d nh]
+  bf16* hn;         // [M, H]
+  float* rstd2;     // [M]
+  bf16* gu;         // [M, 2 F]
+  bf16* act;        // [M, F]
+};
+
+struct Slot {
+  std::vector<float*> x;  // nl + 1 residual-stream buffers, x[0] = stage input
+  std::vector<LayerActs> layers;
+  bf16* xf = nullptr;     // last stage: final-norm output
+  float* rstdf = nullptr;
+  bf16* dlogits = nullptr;
+};
+
+struct TensorPtrs {
+  float* p32 = nullptr;
+  bf16* p16 = nullptr;
+  float* g32 = nullptr;
+  int64_t rows = 0, cols = 0, row0 = 0, count = 0, offset = 0;
+  int spec = -1;
+};
+
+}  // namespace
+
+class Executor {
+ public:
+  Layout L;
+  ExecConfig cfg;
+  int rank = 0, world = 1, device = 0;
+  RankRole role;
+  // model shapes for this rank
+  int64_t H = 0, S = 0, d = 0, nh = 0, F = 0, Vr = 0, v0 = 0, mb = 0, M = 0, nl = 0;
+  int64_t qkvw = 0, kr = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  CUgreenCtx green = nullptr;
+  int sm_total = 0, sm_applied = 0;
+  std::string sm_mode = "none";
+  ncclComm_t world_comm = nullptr;
+  std::vector<ncclComm_t> comms;  // per Layout::comm_sets index (null if not a member)
+  Arena arena;
+  // flat parameter state
+  float *P32 = nullptr, *G32 = nullptr, *Mo = nullptr, *Vo = nullptr;
+  bf16 *P16 = nullptr, *G16 = nullptr;
+  std::map<std::string, TensorPtrs> named;
+  std::vector<TensorPtrs> by_layer[16];
+  // per-layer tensor pointers (local layer index)
+  struct LayerW {
+    TensorPtrs attn_norm, wqkv, wo, mlp_norm, wgu, wdown;
+  };
+  std::vector<LayerW> lw;
+  TensorPtrs embed, final_norm, lm_head;
+  // activations
+  std::vector<Slot> slots;
+  int n_slots = 0;
+  // scratch
+  float *scores = nullptr, *dP = nullptr, *logits = nullptr;
+  bf16 *dS = nullptr, *ypart = nullptr, *da = nullptr, *dgu = nullptr, *dattn = nullptr,
+       *dqkv = nullptr, *dy16 = nullptr;
+  float *dx[2] = {nullptr, nullptr}, *ce_scr = nullptr, *loss_acc = nullptr, *loss_host = nullptr;
+  bf16* dxb = nullptr;
+  int32_t* tokens = nullptr;
+  int32_t* tokens_pinned = nullptr;
+  float* idle_loss_ = nullptr;
+  float* recv_buf = nullptr;  // fwd activations received (fp32 [M,H]) go into slot x[0]
+  int64_t step_index = 0;
+  // stats
+  cudaEvent_t ev[6] = {};
+  float phase_ms[5] = {0, 0, 0, 0, 0};
+  int64_t launches_step = 0, launches_total = 0;
+  int64_t nccl_calls_step = 0;
+  float last_loss = 0.f;
+
+  ~Executor() { teardown(); }
+
+  void teardown() {
+    for (auto& c : comms)
+      if (c) ncclCommDestroy(c);
+    comms.clear();
+    if (world_comm) ncclCommDestroy(world_comm);
+    world_comm = nullptr;
+    arena.release();
+    if (idle_loss_) cudaFree(idle_loss_);
+    idle_loss_ = nullptr;
+    if (tokens_pinned) cudaFreeHost(tokens_pinned);
+    tokens_pinned = nullptr;
+    if (loss_host) cudaFreeHost(loss_host);
+    loss_host = nullptr;
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+    stream = nullptr;
+  }
+
+  // ------------------------------------------------------------ setup
+  void init(const std::string& cj, const std::string& mj, const std::string& pj,
+            const std::string& xj, int r, int w, int dev, const void* uid, size_t uid_len) {
+    cfg = parse_exec_config(xj);
+    L = build_layout(cj, mj, pj);
+    if (w != L.world_size)
+      throw InvalidArgument("world size " + std::to_string(w) + " does not match the cluster's " +
+                            std::to_string(L.world_size) + " devices");
+    if (r < 0 || r >= w) throw InvalidArgument("world rank out of range");
+    rank = r;
+    world = w;
+    device = dev;
+    role = L.roles[size_t(r)];
+    const Model& m = L.model;
+    H = m.hidden_dim;
+    S = m.seq_len;
+    d = m.head_dim();
+    if (role.active) {
+      nh = role.heads.size();
+      F = 64 * role.ffn_chunks.size();
+      Vr = 64 * role.vocab_chunks.size();
+      v0 = 64 * role.vocab_chunks.begin;
+      mb = role.micro_batch;
+      M = mb * S;
+      nl = role.layer_count;
+      qkvw = 3 * d * nh;
+      kr = d * nh;
+    }
+    if (cfg.validate_only) return;
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw CudaError("no CUDA device available (there is no CPU path)");
+    HX_CUDA(cudaSetDevice(dev));
+    HX_CUDA(cudaDeviceGetAttribute(&sm_total, cudaDevAttrMultiProcessorCount, dev));
+    setup_stream();
+    for (auto& e : ev) HX_CUDA(cudaEventCreate(&e));
+    setup_comms(uid, uid_len);
+    if (role.active) {
+      allocate();
+      init_params();
+    } else {
+      HX_CUDA(cudaMalloc(&idle_loss_, 256));
+      loss_acc = idle_loss_;
+      HX_CUDA(cudaMallocHost(&loss_host, 64));
+    }
+    HX_CUDA(cudaStreamSynchronize(stream));
+  }
+
+  // SM cap: green context over sm_fraction * SMs (rounded to the driver's split
+  // granularity); "cta" caps only the persistent GEMM grid; "none" disables.
+  void setup_stream() {
+    int want = role.sm_count > 0 ? role.sm_count
+                                 : int(std::lround(role.sm_fraction * double(sm_total)));
+    want = std::max(1, std::min(want, sm_total));
+    sm_applied = sm_total;
+    if (cfg.sm_cap == "green" && want < sm_total) {
+      if (make_green_stream(want)) {
+        sm_mode = "green";
+        return;
+      }
+    }
+    HX_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    own_stream = true;
+    if ((cfg.sm_cap == "cta" || cfg.sm_cap == "green") && want < sm_total) {
+      gemm_set_sm_limit(want);
+      sm_applied = want;
+      sm_mode = "cta";
+    } else {
+      gemm_set_sm_limit(0);
+    }
+  }
+
+  template <typename T>
+  static T drv(const char* name) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return reinterpret_cast<T>(fn);
+  }
+
+  bool make_green_stream(int want) {
+    auto pGet = drv<PFN_cuDeviceGet>("cuDeviceGet");
+    auto pRes = drv<PFN_cuDeviceGetDevResource>("cuDeviceGetDevResource");
+    auto pSplit = drv<PFN_cuDevSmResourceSplitByCount>("cuDevSmResourceSplitByCount");
+    auto pDesc = drv<PFN_cuDevResourceGenerateDesc>("cuDevResourceGenerateDesc");
+    auto pCreate = drv<PFN_cuGreenCtxCreate>("cuGreenCtxCreate");
+    auto pStream = drv<PFN_cuGreenCtxStreamCreate>("cuGreenCtxStreamCreate");
+    if (!pGet || !pRes || !pSplit || !pDesc || !pCreate || !pStream) return false;
+    cudaFree(nullptr);  // make sure the primary context exists
+    CUdevice cd;
+    if (pGet(&cd, device) != CUDA_SUCCESS) return false;
+    CUdevResource all;
+    if (pRes(cd, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) return false;
+    CUdevResource part, rest;
+    unsigned int groups = 1;
+    if (pSplit(&part, &groups, &all, &rest, 0, unsigned(want)) != CUDA_SUCCESS || groups != 1)
+      return false;
+    CUdevResourceDesc desc;
+    if (pDesc(&desc, &part, 1) != CUDA_SUCCESS) return false;
+    if (pCreate(&green, desc, cd, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) return false;
+    CUstream s;
+    if (pStream(&s, green, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) return false;
+    stream = reinterpret_cast<cudaStream_t>(s);
+    own_stream = true;
+    sm_applied = int(part.sm.smCount);
+    gemm_set_sm_limit(sm_applied);
+    return true;
+  }
+
+  void setup_comms(const void* uid, size_t uid_len) {
+    comms.assign(L.comm_sets.size(), nullptr);
+    if (world == 1) return;
+    if (!uid || uid_len < sizeof(ncclUniqueId))
+      throw InvalidArgument("world_size > 1 needs an NCCL unique id");
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof(id));
+    HX_NCCL(ncclCommInitRank(&world_comm, world, id, rank));
+    for (size_t i = 0; i < L.comm_sets.size(); ++i) {
+      const auto& set = L.comm_sets[i];
+      auto it = std::find(set.begin(), set.end(), rank);
+      int color = it == set.end() ? NCCL_SPLIT_NOCOLOR : 0;
+      int key = it == set.end() ? 0 : int(it - set.begin());
+      ncclComm_t c = nullptr;
+      HX_NCCL(ncclCommSplit(world_comm, color, key, &c, nullptr));
+      comms[i] = c;
+    }
+  }
+
+  // ------------------------------------------------------------ memory
+  void allocate() {
+    const int64_t P = role.param_count;
+    const bool need_g16 = !L.dp_buckets[size_t(rank)].empty() && cfg.dp_comm_dtype == "bf16";
+    n_slots = int(std::min<int64_t>(role.n_mb, role.stage_count - role.stage));
+    n_slots = std::max(n_slots, 1);
+    const int64_t SS = mb * nh * S * S;
+    // parameters
+    arena.reserve(P * 4 * 4);            // P32, G32, M, V
+    arena.reserve(P * 2);                // P16
+    if (need_g16) arena.reserve(P * 2);  // DP comm buffer
+    // activations per slot
+    for (int s = 0; s < n_slots; ++s) {
+      for (int64_t l = 0; l <= nl; ++l) arena.reserve(M * H * 4);
+      for (int64_t l = 0; l < nl; ++l) {
+        arena.reserve(M * H * 4);                  // x_mid
+        arena.reserve(M * H * 2 * 2);              // xn, hn
+        arena.reserve(M * 4 * 2);                  // rstd1, rstd2
+        arena.reserve(M * qkvw * 2);               // qkv
+        arena.reserve(SS * 2);                     // P
+        arena.reserve(M * kr * 2);                 // attn
+        arena.reserve(M * 2 * F * 2 + M * F * 2);  // gu, act
+      }
+      if (role.last_stage) {
+        arena.reserve(M * H * 2 + M * 4);
+        arena.reserve(M * Vr * 2);
+      }
+    }
+    // scratch
+    arena.reserve(SS * 4 * 2);  // scores, dP
+    arena.reserve(SS * 2);      // dS
+    arena.reserve(M * H * 2);   // ypart
+    arena.reserve(M * F * 2 + M * 2 * F * 2 + M * kr * 2 + M * qkvw * 2);
+    arena.reserve(M * H * 4 * 2 + M * H * 2 + M * H * 2);  // dx ping-pong, dxb, dy16
+    if (role.last_stage) arena.reserve(M * Vr * 4 + 5 * M * 4);
+    arena.reserve(256);                                    // loss
+    arena.reserve(role.batch * (S + 1) * 4);               // tokens
+    arena.commit();
+
+    P32 = arena.take<float>(P);
+    G32 = arena.take<float>(P);
+    Mo = arena.take<float>(P);
+    Vo = arena.take<float>(P);
+    P16 = arena.take<bf16>(P);
+    if (need_g16) G16 = arena.take<bf16>(P);
+    slots.resize(size_t(n_slots));
+    for (auto& sl : slots) {
+      for (int64_t l = 0; l <= nl; ++l) sl.x.push_back(arena.take<float>(M * H));
+      for (int64_t l = 0; l < nl; ++l) {
+        LayerActs a;
+        a.x_mid = arena.take<float>(M * H);
+        a.xn = arena.take<bf16>(M * H);
+        a.hn = arena.take<bf16>(M * H);
+        a.rstd1 = arena.take<float>(M);
+        a.rstd2 = arena.take<float>(M);
+        a.qkv = arena.take<bf16>(M * qkvw);
+        a.P = arena.take<bf16>(SS);
+        a.attn = arena.take<bf16>(M * kr);
+        a.gu = arena.take<bf16>(M * 2 * F);
+        a.act = arena.take<bf16>(M * F);
+        sl.layers.push_back(a);
+      }
+      if (role.last_stage) {
+        sl.xf = arena.take<bf16>(M * H);
+        sl.rstdf = arena.take<float>(M);
+        sl.dlogits = arena.take<bf16>(M * Vr);
+      }
+    }
+    scores = arena.take<float>(SS);
+    dP = arena.take<float>(SS);
+    dS = arena.take<bf16>(SS);
+    ypart = arena.take<bf16>(M * H);
+    da = arena.take<bf16>(M * F);
+    dgu = arena.take<bf16>(M * 2 * F);
+    dattn = arena.take<bf16>(M * kr);
+    dqkv = arena.take<bf16>(M * qkvw);
+    dx[0] = arena.take<float>(M * H);
+    dx[1] = arena.take<float>(M * H);
+    dxb = arena.take<bf16>(M * H);
+    dy16 = arena.take<bf16>(M * H);
+    if (role.last_stage) {
+      logits = arena.take<float>(M * Vr);
+      ce_scr = arena.take<float>(5 * M);
+    }
+    loss_acc = arena.take<float>(64);
+    tokens = arena.take<int32_t>(role.batch * (S + 1));
+    HX_CUDA(cudaMallocHost(&tokens_pinned, size_t(role.batch * (S + 1)) * 4));
+    HX_CUDA(cudaMallocHost(&loss_host, 64));
+
+    // tensor pointers
+    lw.assign(size_t(nl), LayerW{});
+    for (const auto& rt : role.tensors) {
+      const TensorSpec& ts = L.tensors[size_t(rt.spec)];
+      TensorPtrs tp;
+      tp.p32 = P32 + rt.offset;
+      tp.p16 = P16 + rt.offset;
+      tp.g32 = G32 + rt.offset;
+      tp.rows = rt.rows;
+      tp.cols = ts.cols;
+      tp.row0 = rt.row0;
+      tp.count = rt.rows * ts.cols;
+      tp.offset = rt.offset;
+      tp.spec = rt.spec;
+      named[ts.name] = tp;
+      if (ts.layer >= 0) {
+        LayerW& w = lw[size_t(ts.layer - role.layer_start)];
+        switch (ts.id) {
+          case kAttnNorm: w.attn_norm = tp; break;
+          case kWqkv: w.wqkv = tp; break;
+          case kWo: w.wo = tp; break;
+          case kMlpNorm: w.mlp_norm = tp; break;
+          case kWgu: w.wgu = tp; break;
+          case kWdown: w.wdown = tp; break;
+        }
+      } else if (ts.id == kEmbed) {
+        embed = tp;
+      } else if (ts.id == kFinalNorm) {
+        final_norm = tp;
+      } else if (ts.id == kLmHead) {
+        lm_head = tp;
+      }
+    }
+  }
+
+  void init_params() {
+    for (const auto& rt : role.tensors) {
+      const TensorSpec& ts = L.tensors[size_t(rt.spec)];
+      const TensorPtrs& tp = named[ts.name];
+      if (ts.id == kAttnNorm || ts.id == kMlpNorm || ts.id == kFinalNorm) {
+        k_fill(tp.p32, tp.p16, tp.count, 1.f, stream);
+      } else {
+        uint64_t seed = mix_seed(cfg.seed, uint64_t(ts.layer + 1), uint64_t(ts.id));
+        k_init_normal(tp.p32, tp.p16, tp.count, tp.row0 * tp.cols, seed, stream);
+      }
+    }
+    HX_CUDA(cudaMemsetAsync(Mo, 0, size_t(role.param_count) * 4, stream));
+    HX_CUDA(cudaMemsetAsync(Vo, 0, size_t(role.param_count) * 4, stream));
+    HX_CUDA(cudaMemsetAsync(G32, 0, size_t(role.param_count) * 4, stream));
+    HX_CUDA(cudaGetLastError());
+  }
+
+  // ------------------------------------------------------------ helpers
+  void kcheck() {
+    ++launches_step;
+    cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) throw CudaError(std::string("kernel launch: ") + cudaGetErrorString(e));
+  }
+
+  void gemm(const GemmDesc& g) {
+    cudaError_t e = gemm_bf16(g, stream);
+    if (e != cudaSuccess) throw CudaError(std::string("gemm: ") + cudaGetErrorString(e));
+    ++launches_step;
+  }
+
+  // plain 2D GEMM helper
+  GemmDesc g2(int64_t Mm, int64_t Nn, int64_t Kk, const void* A, int amn, int64_t lda,
+              const void* B, int bmn, int64_t ldb, void* C, int64_t ldc, int c32) {
+    GemmDesc g;
+    g.M = int(Mm);
+    g.N = int(Nn);
+    g.K = int(Kk);
+    g.A = {A, amn, lda, 0, 0};
+    g.B = {B, bmn, ldb, 0, 0};
+    g.C = C;
+    g.ldc = ldc;
+    g.c_fp32 = c32;
+    return g;
+  }
+
+  ncclComm_t tp_comm() const {
+    int c = L.tp_comm[size_t(rank)];
+    return c >= 0 ? comms[size_t(c)] : nullptr;
+  }
+
+  void tp_allreduce_bf16(bf16* buf, int64_t n) {
+    if (role.tp <= 1) return;
+    HX_NCCL(ncclAllReduce(buf, buf, size_t(n), ncclBfloat16, ncclSum, tp_comm(), stream));
+    ++nccl_calls_step;
+  }
+
+  void tp_allreduce_f32(const float* in, float* out, int64_t n, ncclRedOp_t op) {
+    if (role.tp <= 1) return;
+    HX_NCCL(ncclAllReduce(in, out, size_t(n), ncclFloat32, op, tp_comm(), stream));
+    ++nccl_calls_step;
+  }
+
+  int32_t* tok_of(int64_t mbi) { return tokens + mbi * mb * (S + 1); }
+
+  // ------------------------------------------------------------ forward
+  void layer_fwd(Slot& sl, int64_t l) {
+    LayerActs& a = sl.layers[size_t(l)];
+    const LayerW& w = lw[size_t(l)];
+    float* x_in = sl.x[size_t(l)];
+    float* x_out = sl.x[size_t(l + 1)];
+    const float eps = float(L.model.norm_eps);
+    // attention block
+    k_rmsnorm_fwd(x_in, nullptr, nullptr, w.attn_norm.p32, a.xn, a.rstd1, int(M), int(H), eps, stream);
+    kcheck();
+    gemm(g2(M, qkvw, H, a.xn, 0, H, w.wqkv.p16, 0, H, a.qkv, qkvw, 0));
+    k_rope(a.qkv, int(M), int(S), int(nh), int(d), float(L.model.rope_theta), 0, stream);
+    kcheck();
+    attention_fwd(a);
+    if (role.tp == 1) {
+      GemmDesc g = g2(M, H, kr, a.attn, 0, kr, w.wo.p16, 1, H, a.x_mid, H, 1);
+      g.R = x_in;
+      gemm(g);
+      k_rmsnorm_fwd(a.x_mid, nullptr, nullptr, w.mlp_norm.p32, a.hn, a.rstd2, int(M), int(H), eps, stream);
+      kcheck();
+    } else {
+      gemm(g2(M, H, kr, a.attn, 0, kr, w.wo.p16, 1, H, ypart, H, 0));
+      tp_allreduce_bf16(ypart, M * H);
+      k_rmsnorm_fwd(x_in, ypart, a.x_mid, w.mlp_norm.p32, a.hn, a.rstd2, int(M), int(H), eps, stream);
+      kcheck();
+    }
+    // MLP block
+    gemm(g2(M, 2 * F, H, a.hn, 0, H, w.wgu.p16, 0, H, a.gu, 2 * F, 0));
+    k_swiglu_fwd(a.gu, a.act, int(M), int(F), stream);
+    kcheck();
+    if (role.tp == 1) {
+      GemmDesc g = g2(M, H, F, a.act, 0, F, w.wdown.p16, 1, H, x_out, H, 1);
+      g.R = a.x_mid;
+      gemm(g);
+    } else {
+      gemm(g2(M, H, F, a.act, 0, F, w.wdown.p16, 1, H, ypart, H, 0));
+      tp_allreduce_bf16(ypart, M * H);
+      k_residual_add(a.x_mid, ypart, x_out, M * H, stream);
+      kcheck();
+    }
+  }
+
+  // per (sample b, head h): scores = q k^T / sqrt(d) (causal tiles), P = softmax,
+  // attn = P v -- batched over z = h + nh * b straight out of the QKV buffer
+  void attention_fwd(LayerActs& a) {
+    const int64_t SS2 = S * S;
+    GemmDesc g;
+    g.M = int(S);
+    g.N = int(S);
+    g.K = int(d);
+    g.nb1 = int(nh);
+    g.nb2 = int(mb);
+    g.A = {a.qkv, 0, qkvw, 3 * d, S * qkvw};
+    g.B = {a.qkv + d, 0, qkvw, 3 * d, S * qkvw};
+    g.C = scores;
+    g.ldc = S;
+    g.cbs1 = SS2;
+    g.cbs2 = nh * SS2;
+    g.c_fp32 = 1;
+    g.alpha = 1.f / std::sqrt(float(d));
+    g.causal = kCausalSkipUpper;
+    gemm(g);
+    k_softmax_fwd(scores, a.P, int(S), int(mb * nh), stream);
+    kcheck();
+    GemmDesc o;
+    o.M = int(S);
+    o.N = int(d);
+    o.K = int(S);
+    o.nb1 = int(nh);
+    o.nb2 = int(mb);
+    o.A = {a.P, 0, S, SS2, nh * SS2};
+    o.B = {a.qkv + 2 * d, 1, qkvw, 3 * d, S * qkvw};
+    o.C = a.attn;
+    o.ldc = kr;
+    o.cbs1 = d;
+    o.cbs2 = S * kr;
+    o.causal = kCausalKLower;
+    gemm(o);
+  }
+
+  void head_fwd(Slot& sl, int64_t mbi) {
+    const float eps = float(L.model.norm_eps);
+    k_rmsnorm_fwd(sl.x[size_t(nl)], nullptr, nullptr, final_norm.p32, sl.xf, sl.rstdf, int(M), int(H), eps, stream);
+    kcheck();
+    gemm(g2(M, Vr, H, sl.xf, 0, H, lm_head.p16, 0, H, logits, Vr, 1));
+    float* lmax = ce_scr;
+    float* lsum = ce_scr + M;
+    float* st2 = ce_scr + 2 * M;
+    float* gmax = ce_scr + 4 * M;
+    const int32_t* tk = tok_of(mbi);
+    k_ce_stats(logits, int(Vr), int(v0), tk, int(M), int(S), lmax, lsum, st2, stream);
+    kcheck();
+    if (role.tp > 1) {
+      tp_allreduce_f32(lmax, gmax, M, ncclMax);
+      k_ce_rescale(lmax, lsum, gmax, st2, int(M), stream);
+      kcheck();
+      tp_allreduce_f32(st2, st2, 2 * M, ncclSum);
+    } else {
+      HX_CUDA(cudaMemcpyAsync(gmax, lmax, size_t(M) * 4, cudaMemcpyDeviceToDevice, stream));
+    }
+    const float inv_count = 1.f / float(role.batch * S);
+    k_ce_finish(logits, int(Vr), int(v0), tk, int(M), int(S), gmax, st2, inv_count, sl.dlogits,
+                loss_acc, stream);
+    kcheck();
+  }
+
+  void forward(int64_t mbi, Slot& sl) {
+    if (role.first_stage) {
+      k_embed_fwd(tok_of(mbi), embed.p32, sl.x[0], int(M), int(S), int(H), stream);
+      kcheck();
+    }
+    for (int64_t l = 0; l < nl; ++l) layer_fwd(sl, l);
+    if (role.last_stage) head_fwd(sl, mbi);
+  }
+
+  // ------------------------------------------------------------ backward
+  // dxo: fp32 grad of the layer output (+ bf16 copy dxob); writes dx_in/dxb_in
+  void layer_bwd(Slot& sl, int64_t l, const float* dxo, const bf16* dxob, float* dxi, bf16* dxib) {
+    LayerActs& a = sl.layers[size_t(l)];
+    const LayerW& w = lw[size_t(l)];
+    const bool first_mb = accum_first_;
+    // MLP: down projection
+    gemm(g2(M, F, H, dxob, 0, H, w.wdown.p16, 0, H, da, F, 0));
+    {
+      GemmDesc g = g2(F, H, M, a.act, 1, F, dxob, 1, H, w.wdown.g32, H, 1);
+      g.beta = first_mb ? 0 : 1;
+      gemm(g);
+    }
+    k_swiglu_bwd(a.gu, da, dgu, int(M), int(F), stream);
+    kcheck();
+    gemm(g2(M, H, 2 * F, dgu, 0, 2 * F, w.wgu.p16, 1, H, dy16, H, 0));
+    {
+      GemmDesc g = g2(2 * F, H, M, dgu, 1, 2 * F, a.hn, 1, H, w.wgu.g32, H, 1);
+      g.beta = first_mb ? 0 : 1;
+      gemm(g);
+    }
+    tp_allreduce_bf16(dy16, M * H);
+    // dx_mid = dx_out + rmsnorm_bwd(dhn);  (reuse dxi as dx_mid storage)
+    float* dxm = dxi;
+    bf16* dxmb = dxib;
+    k_rmsnorm_bwd(dy16, nullptr, a.x_mid, a.rstd2, w.mlp_norm.p32, dxo, dxm, dxmb, w.mlp_norm.g32,
+                  int(M), int(H), stream);
+    kcheck();
+    // attention: O projection
+    gemm(g2(M, kr, H, dxmb, 0, H, w.wo.p16, 0, H, dattn, kr, 0));
+    {
+      GemmDesc g = g2(kr, H, M, a.attn, 1, kr, dxmb, 1, H, w.wo.g32, H, 1);
+      g.beta = first_mb ? 0 : 1;
+      gemm(g);
+    }
+    attention_bwd(a);
+    k_rope(dqkv, int(M), int(S), int(nh), int(d), float(L.model.rope_theta), 1, stream);
+    kcheck();
+    gemm(g2(M, H, qkvw, dqkv, 0, qkvw, w.wqkv.p16, 1, H, dy16, H, 0));
+    {
+      GemmDesc g = g2(qkvw, H, M, dqkv, 1, qkvw, a.xn, 1, H, w.wqkv.g32, H, 1);
+      g.beta = first_mb ? 0 : 1;
+      gemm(g);
+    }
+    tp_allreduce_bf16(dy16, M * H);
+    // dx_in = dx_mid + rmsnorm_bwd(dxn): in place over dx_mid (row-local)
+    k_rmsnorm_bwd(dy16, nullptr, sl.x[size_t(l)], a.rstd1, w.attn_norm.p32, dxm, dxi, dxib,
+                  w.attn_norm.g32, int(M), int(H), stream);
+    kcheck();
+  }
+
+  void attention_bwd(LayerActs& a) {
+    const int64_t SS2 = S * S;
+    // dP = dO V^T
+    GemmDesc g;
+    g.M = int(S);
+    g.N = int(S);
+    g.K = int(d);
+    g.nb1 = int(nh);
+    g.nb2 = int(mb);
+    g.A = {dattn, 0, kr, d, S * kr};
+    g.B = {a.qkv + 2 * d, 0, qkvw, 3 * d, S * qkvw};
+    g.C = dP;
+    g.ldc = S;
+    g.cbs1 = SS2;
+    g.cbs2 = nh * SS2;
+    g.c_fp32 = 1;
+    g.causal = kCausalSkipUpper;
+    gemm(g);
+    k_softmax_bwd(a.P, dP, dS, 1.f / std::sqrt(float(d)), int(S), int(mb * nh), stream);
+    kcheck();
+    // dQ = dS K
+    GemmDesc q;
+    q.M = int(S);
+    q.N = int(d);
+    q.K = int(S);
+    q.nb1 = int(nh);
+    q.nb2 = int(mb);
+    q.A = {dS, 0, S, SS2, nh * SS2};
+    q.B = {a.qkv + d, 1, qkvw, 3 * d, S * qkvw};
+    q.C = dqkv;
+    q.ldc = qkvw;
+    q.cbs1 = 3 * d;
+    q.cbs2 = S * qkvw;
+    q.causal = kCausalKLower;
+    gemm(q);
+    // dK = dS^T Q
+    GemmDesc k = q;
+    k.A = {dS, 1, S, SS2, nh * SS2};
+    k.B = {a.qkv, 1, qkvw, 3 * d, S * qkvw};
+    k.C = dqkv + d;
+    k.causal = kCausalKUpper;
+    gemm(k);
+    // dV = P^T dO
+    GemmDesc v = q;
+    v.A = {a.P, 1, S, SS2, nh * SS2};
+    v.B = {dattn, 1, kr, d, S * kr};
+    v.C = dqkv + 2 * d;
+    v.causal = kCausalKUpper;
+    gemm(v);
+  }
+
+  // backward of one micro-batch; dx_top (fp32) is the grad of the stage output
+  // (received), or null on the last stage (starts from dlogits)
+  void backward(int64_t mbi, Slot& sl, float* dx_top) {
+    float* cur = dx[0];
+    float* nxt = dx[1];
+    bf16* curb = dxb;
+    if (role.last_stage) {
+      gemm(g2(M, H, Vr, sl.dlogits, 0, Vr, lm_head.p16, 1, H, dy16, H, 0));
+      GemmDesc g = g2(Vr, H, M, sl.dlogits, 1, Vr, sl.xf, 1, H, lm_head.g32, H, 1);
+      g.beta = accum_first_ ? 0 : 1;
+      gemm(g);
+      tp_allreduce_bf16(dy16, M * H);
+      k_rmsnorm_bwd(dy16, nullptr, sl.x[size_t(nl)], sl.rstdf, final_norm.p32, nullptr, cur, curb,
+                    final_norm.g32, int(M), int(H), stream);
+      kcheck();
+    } else {
+      HX_CUDA(cudaMemcpyAsync(cur, dx_top, size_t(M * H) * 4, cudaMemcpyDeviceToDevice, stream));
+      k_cast_bf16(cur, curb, M * H, stream);
+      kcheck();
+    }
+    for (int64_t l = nl - 1; l >= 0; --l) {
+      // dxi aliases the ping-pong partner; dxb reused in place (row-local ops)
+      layer_bwd(sl, l, cur, curb, nxt, curb);
+      std::swap(cur, nxt);
+    }
+    if (role.first_stage) {
+      k_embed_bwd(tok_of(mbi), cur, embed.g32, int(M), int(S), int(H), stream);
+      kcheck();
+    }
+    bwd_out_ = cur;
+  }
+
+  // ------------------------------------------------------------ PP comm
+  void send_fwd(Slot& sl) {
+    for (int peer : role.fwd_send_to) {
+      HX_NCCL(ncclSend(sl.x[size_t(nl)], size_t(M * H), ncclFloat32, peer, world_comm, stream));
+      ++nccl_calls_step;
+    }
+  }
+  void recv_fwd(Slot& sl) {
+    if (role.fwd_recv_from >= 0) {
+      HX_NCCL(ncclRecv(sl.x[0], size_t(M * H), ncclFloat32, role.fwd_recv_from, world_comm, stream));
+      ++nccl_calls_step;
+    }
+  }
+  void send_bwd(const float* g) {
+    for (int peer : role.bwd_send_to) {
+      HX_NCCL(ncclSend(g, size_t(M * H), ncclFloat32, peer, world_comm, stream));
+      ++nccl_calls_step;
+    }
+  }
+  void recv_bwd(float* g) {
+    if (role.bwd_recv_from >= 0) {
+      HX_NCCL(ncclRecv(g, size_t(M * H), ncclFloat32, role.bwd_recv_from, world_comm, stream));
+      ++nccl_calls_step;
+    }
+  }
+
+  // ------------------------------------------------------------ step
+  bool accum_first_ = true;
+  float* bwd_out_ = nullptr;
+  float* grad_in_ = nullptr;  // received grad buffer (reuses scores-free scratch)
+
+  void run_pipeline() {
+    const int64_t n = role.n_mb;
+    const int P = role.stage_count;
+    const int j = role.stage;
+    const int64_t warm = std::min<int64_t>(P - j - 1, n);
+    const int64_t rem = n - warm;
+    float* grecv = dx[1];  // grads from the next stage land here before backward copies them
+    // we receive into a dedicated region: use ypart-sized fp32? dx[1] is free between
+    // backward passes; backward() copies it into dx[0] first.
+    auto slot_of = [&](int64_t mbi) -> Slot& { return slots[size_t(mbi % n_slots)]; };
+    int64_t next_bwd = 0;
+    auto do_bwd = [&](int64_t mbi) {
+      accum_first_ = next_bwd == 0;
+      backward(mbi, slot_of(mbi), grecv);
+      ++next_bwd;
+    };
+    // warm-up forwards
+    for (int64_t i = 0; i < warm; ++i) {
+      Slot& sl = slot_of(i);
+      recv_fwd(sl);
+      forward(i, sl);
+      send_fwd(sl);
+    }
+    if (rem > 0) recv_fwd(slot_of(warm));
+    for (int64_t i = 0; i < rem; ++i) {
+      const int64_t f = warm + i;
+      Slot& sl = slot_of(f);
+      forward(f, sl);
+      // send activation + receive the grad for micro-batch i (grouped)
+      HX_NCCL(ncclGroupStart());
+      send_fwd(sl);
+      recv_bwd(grecv);
+      HX_NCCL(ncclGroupEnd());
+      do_bwd(i);
+      HX_NCCL(ncclGroupStart());
+      send_bwd(bwd_out_);
+      if (i + 1 < rem) recv_fwd(slot_of(f + 1));
+      HX_NCCL(ncclGroupEnd());
+    }
+    for (int64_t i = rem; i < n; ++i) {
+      recv_bwd(grecv);
+      do_bwd(i);
+      send_bwd(bwd_out_);
+    }
+  }
+
+  void dp_sync_and_update() {
+    const auto& buckets = L.dp_buckets[size_t(rank)];
+    cudaEventRecord(ev[2], stream);
+    const bool bf = G16 != nullptr;
+    // 1. weight by samples: scale = (batch_i / global_batch) / multiplicity, fused
+    //    with the bf16 cast for tensors that take part in a DP allreduce
+    for (const auto& rt : role.tensors) {
+      const int64_t cnt = rt.rows * L.tensors[size_t(rt.spec)].cols;
+      if (!covered(rt.offset, cnt)) continue;
+      const float sc = float(role.dp_weight / double(rt.multiplicity));
+      if (bf)
+        k_scale_cast(G32 + rt.offset, G16 + rt.offset, cnt, sc, stream);
+      else
+        k_scale(G32 + rt.offset, cnt, sc, stream);
+      kcheck();
+    }
+    // 2. chunk-matched allreduce, one NCCL call per bucket (grouped)
+    if (!buckets.empty()) {
+      HX_NCCL(ncclGroupStart());
+      for (const auto& b : buckets) {
+        if (bf)
+          HX_NCCL(ncclAllReduce(G16 + b.offset, G16 + b.offset, size_t(b.count), ncclBfloat16,
+                                ncclSum, comms[size_t(b.comm)], stream));
+        else
+          HX_NCCL(ncclAllReduce(G32 + b.offset, G32 + b.offset, size_t(b.count), ncclFloat32,
+                                ncclSum, comms[size_t(b.comm)], stream));
+        ++nccl_calls_step;
+      }
+      HX_NCCL(ncclGroupEnd());
+    }
+    cudaEventRecord(ev[3], stream);
+    // 3. AdamW per tensor (weight decay only on matrices)
+    const float t = float(step_index + 1);
+    const float bc1 = 1.f - std::pow(cfg.beta1, t);
+    const float bc2 = 1.f - std::pow(cfg.beta2, t);
+    for (const auto& rt : role.tensors) {
+      const TensorSpec& ts = L.tensors[size_t(rt.spec)];
+      const int64_t cnt = rt.rows * ts.cols;
+      const float wd = ts.decay ? cfg.weight_decay : 0.f;
+      const bool cov = covered(rt.offset, cnt);
+      const bf16* g16 = cov && bf ? G16 + rt.offset : nullptr;
+      const float* g32 = g16 ? nullptr : G32 + rt.offset;
+      const float gscale = cov ? 1.f : float(role.dp_weight / double(rt.multiplicity));
+      k_adamw(P32 + rt.offset, P16 + rt.offset, Mo + rt.offset, Vo + rt.offset, g16, g32, cnt,
+              gscale, cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, wd, bc1, bc2, stream);
+      kcheck();
+    }
+    cudaEventRecord(ev[4], stream);
+  }
+
+  // is [off, off+cnt) fully covered by this rank's DP buckets? (buckets never
+  // partially cover a tensor unless its shard boundaries differ across pipelines,
+  // in which case the uncovered part has a single holder)
+  bool covered(int64_t off, int64_t cnt) const {
+    int64_t c = 0;
+    for (const auto& b : L.dp_buckets[size_t(rank)]) {
+      int64_t lo = std::max(off, b.offset), hi = std::min(off + cnt, b.offset + b.count);
+      if (hi > lo) c += hi - lo;
+    }
+    return c == cnt;
+  }
+
+  void step_enqueue() {
+    if (!role.active) {
+      // idle device: still joins the world loss reduction (contributes 0)
+      HX_CUDA(cudaMemsetAsync(loss_acc, 0, 4, stream));
+      finish_loss();
+      ++step_index;
+      return;
+    }
+    launches_step = 0;
+    nccl_calls_step = 0;
+    cudaEventRecord(ev[0], stream);
+    if (tokens_from_host_ == nullptr && (role.first_stage || role.last_stage)) {
+      k_gen_tokens(tokens, role.batch, int(S), role.sample0, cfg.seed, step_index,
+                   int(L.model.vocab_size), stream);
+      kcheck();
+    }
+    HX_CUDA(cudaMemsetAsync(loss_acc, 0, 4, stream));
+    // zero the atomically-accumulated grads (norm gains, embedding)
+    for (const auto& rt : role.tensors) {
+      const TensorSpec& ts = L.tensors[size_t(rt.spec)];
+      if (ts.id == kAttnNorm || ts.id == kMlpNorm || ts.id == kFinalNorm || ts.id == kEmbed)
+        HX_CUDA(cudaMemsetAsync(G32 + rt.offset, 0, size_t(rt.rows * ts.cols) * 4, stream));
+    }
+    cudaEventRecord(ev[1], stream);
+    run_pipeline();
+    dp_sync_and_update();
+    finish_loss();
+    cudaEventRecord(ev[5], stream);
+    launches_total += launches_step;
+    ++step_index;
+  }
+
+  void finish_loss() {
+    if (world > 1) {
+      HX_NCCL(ncclAllReduce(loss_acc, loss_acc, 1, ncclFloat32, ncclSum, world_comm, stream));
+      ++nccl_calls_step;
+    }
+  }
+
+  cudaStream_t stream_or_default() { return stream; }
+
+  const int32_t* tokens_from_host_ = nullptr;
+
+  void step(const int32_t* host_tokens, size_t n, float* loss_out) {
+    if (role.active && host_tokens) {
+      const size_t need = size_t(role.batch * (S + 1));
+      if (n != need)
+        throw InvalidArgument("tokens: expected " + std::to_string(need) + " values for this pipeline");
+      std::memcpy(tokens_pinned, host_tokens, need * 4);
+      HX_CUDA(cudaMemcpyAsync(tokens, tokens_pinned, need * 4, cudaMemcpyHostToDevice, stream));
+    }
+    tokens_from_host_ = host_tokens;
+    step_enqueue();
+    tokens_from_host_ = nullptr;
+    HX_CUDA(cudaMemcpyAsync(loss_host, loss_acc, 4, cudaMemcpyDeviceToHost, stream));
+    HX_CUDA(cudaStreamSynchronize(stream));
+    last_loss = loss_host[0] / float(L.plan.global_batch * S);
+    if (role.active) collect_times();
+    if (loss_out) *loss_out = last_loss;
+  }
+
+  void collect_times() {
+    float t;
+    if (cudaEventElapsedTime(&t, ev[0], ev[1]) == cudaSuccess) phase_ms[0] = t;
+    if (cudaEventElapsedTime(&t, ev[1], ev[2]) == cudaSuccess) phase_ms[1] = t;
+    if (cudaEventElapsedTime(&t, ev[2], ev[3]) == cudaSuccess) phase_ms[2] = t;
+    if (cudaEventElapsedTime(&t, ev[3], ev[4]) == cudaSuccess) phase_ms[3] = t;
+    if (cudaEventElapsedTime(&t, ev[0], ev[5]) == cudaSuccess) phase_ms[4] = t;
+  }
+
+  std::string stats() const {
+    ojson j;
+    j["rank"] = rank;
+    j["active"] = role.active;
+    j["sm_total"] = sm_total;
+    j["sm_applied"] = sm_applied;
+    j["sm_cap_mode"] = sm_mode;
+    j["sm_fraction"] = role.sm_fraction;
+    j["arena_bytes"] = arena.total();
+    j["activation_slots"] = n_slots;
+    j["param_count"] = role.param_count;
+    j["steps"] = step_index;
+    j["launches_last_step"] = launches_step;
+    j["launches_total"] = launches_total;
+    j["nccl_calls_last_step"] = nccl_calls_step;
+    j["ms"] = {{"prologue", phase_ms[0]}, {"pipeline", phase_ms[1]}, {"dp_sync", phase_ms[2]},
+               {"optimizer", phase_ms[3]}, {"step", phase_ms[4]}};
+    j["last_loss"] = last_loss;
+    return j.dump();
+  }
+};
+
+// ------------------------------------------------------------------ free functions
+Executor* make_executor(const std::string& c, const std::string& m, const std::string& p,
+                        const std::string& x, int r, int w, int dev, const void* uid,
+                        size_t uid_len) {
+  auto* e = new Executor();
+  try {
+    e->init(c, m, p, x, r, w, dev, uid, uid_len);
+  } catch (...) {
+    delete e;
+    throw;
+  }
+  return e;
+}
+
+void executor_step(Executor& e, const int32_t* t, size_t n, float* loss) { e.step(t, n, loss); }
+
+void executor_step_async(Executor& e) {
+  e.tokens_from_host_ = nullptr;
+  e.step_enqueue();
+}
+
+void executor_sync(Executor& e) {
+  if (e.stream) HX_CUDA(cudaStreamSynchronize(e.stream));
+  HX_CUDA(cudaMemcpy(e.loss_host, e.loss_acc, 4, cudaMemcpyDeviceToHost));
+  e.last_loss = e.loss_host[0] / float(e.L.plan.global_batch * e.S);
+  if (e.role.active) e.collect_times();
+}
+
+float executor_last_loss(Executor& e) { return e.last_loss; }
+
+void executor_synth_tokens(const Executor& e, int64_t step, int32_t* out, size_t n) {
+  if (!e.role.active) return;
+  const int64_t S1 = e.S + 1;
+  if (n != size_t(e.role.batch * S1)) throw InvalidArgument("tokens: wrong buffer size");
+  for (int64_t i = 0; i < e.role.batch; ++i) {
+    uint64_t base = mix_seed(e.cfg.seed, kTokenTag, uint64_t(step), uint64_t(e.role.sample0 + i));
+    for (int64_t p = 0; p < S1; ++p)
+      out[i * S1 + p] = int32_t(splitmix64(base + uint64_t(p)) % uint64_t(e.L.model.vocab_size));
+  }
+}
+
+bool executor_tensor_info(const Executor& e, const std::string& name, int64_t* row0,
+                          int64_t* rows, int64_t* cols, int64_t* grows) {
+  for (const auto& ts : e.L.tensors) {
+    if (ts.name != name) continue;
+    *cols = ts.cols;
+    *grows = ts.global_rows;
+    *row0 = 0;
+    *rows = 0;
+    auto it = e.named.find(name);
+    if (it != e.named.end()) {
+      *row0 = it->second.row0;
+      *rows = it->second.rows;
+    }
+    return true;
+  }
+  return false;
+}
+
+void executor_read_tensor(Executor& e, const std::string& name, int which, float* out, size_t n) {
+  auto it = e.named.find(name);
+  if (it == e.named.end()) throw InvalidArgument("tensor not held by this rank: " + name);
+  const TensorPtrs& t = it->second;
+  if (n != size_t(t.count)) throw InvalidArgument("read_tensor: wrong element count");
+  HX_CUDA(cudaStreamSynchronize(e.stream));
+  switch (which) {
+    case 0:
+      HX_CUDA(cudaMemcpy(out, t.p32, n * 4, cudaMemcpyDeviceToHost));
+      break;
+    case 1: {
+      // the gradient AdamW consumed (DP-reduced, sample-weighted)
+      const RankTensor* rt = nullptr;
+      for (const auto& r : e.role.tensors)
+        if (r.spec == t.spec) rt = &r;
+      const bool cov = e.covered(t.offset, t.count);
+      if (cov && e.G16) {
+        std::vector<uint16_t> tmp(n);
+        HX_CUDA(cudaMemcpy(tmp.data(), e.G16 + t.offset, n * 2, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < n; ++i) {
+          uint32_t u = uint32_t(tmp[i]) << 16;
+          std::memcpy(&out[i], &u, 4);
+        }
+      } else {
+        HX_CUDA(cudaMemcpy(out, t.g32, n * 4, cudaMemcpyDeviceToHost));
+        if (!cov) {
+          float sc = float(e.role.dp_weight / double(rt ? rt->multiplicity : 1));
+          for (size_t i = 0; i < n; ++i) out[i] *= sc;
+        }
+      }
+      break;
+    }
+    case 2:
+      HX_CUDA(cudaMemcpy(out, e.Mo + t.offset, n * 4, cudaMemcpyDeviceToHost));
+      break;
+    case 3:
+      HX_CUDA(cudaMemcpy(out, e.Vo + t.offset, n * 4, cudaMemcpyDeviceToHost));
+      break;
+    default:
+      throw InvalidArgument("read_tensor: which must be 0..3");
+  }
+}
+
+std::string executor_stats_json(const Executor& e) { return e.stats(); }
+
+void destroy_executor(Executor* e) { delete e; }
+
+}  // namespace hexexec

@@ -37,6 +37,7 @@ struct GemmDesc {
   GemmOperand A, B;
   void* C = nullptr;
   long long ldc = 0, cbs1 = 0, cbs2 = 0;
+  const float* R = nullptr;  // optional fp32 residual, same layout as C: C = alpha*acc + R
   int c_fp32 = 0;  // 1: fp32 output, 0: bf16 output
   int beta = 0;    // 1: C += alpha*acc (fp32 C only)
   float alpha = 1.f;

@@ -30,6 +30,7 @@ constexpr int kThreads = 256;
 
 struct EpiParams {
   void* C;
+  const float* R;
   long long ldc, cbs1, cbs2;
   int M, N, K, nb1, nb2;
   int c_fp32, beta;
@@ -225,6 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool full_chunk = col + 32 <= p.N;
         if (p.c_fp32) {
           float* out = reinterpret_cast<float*>(p.C) + cbase + col;
+          const float* res = p.R ? p.R + cbase + col : nullptr;
           if (full_chunk && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
             float4* o4 = reinterpret_cast<float4*>(out);
 #pragma unroll
@@ -234,10 +236,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float4 o = o4[i];
                 w.x += o.x; w.y += o.y; w.z += o.z; w.w += o.w;
               }
+              if (res) {
+                float4 o = reinterpret_cast<const float4*>(res)[i];
+                w.x += o.x; w.y += o.y; w.z += o.z; w.w += o.w;
+              }
               o4[i] = w;
             }
           } else {
-            for (int i = 0; i < 32 && col + i < p.N; ++i) out[i] = p.beta ? out[i] + v[i] : v[i];
+            for (int i = 0; i < 32 && col + i < p.N; ++i)
+              out[i] = (p.beta ? out[i] : 0.f) + (res ? res[i] : 0.f) + v[i];
           }
         } else {
           __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.C) + cbase + col;
@@ -368,6 +375,8 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream) {
   if (!ok) return cudaErrorInvalidValue;
   EpiParams p;
   p.C = d.C;
+  p.R = d.R;
+  if (d.R && !d.c_fp32) return cudaErrorInvalidValue;
   p.ldc = d.ldc;
   p.cbs1 = d.cbs1;
   p.cbs2 = d.cbs2;

@@ -398,6 +398,12 @@ __global__ void scale_cast_kernel(const float* g, bf16* out, long long n, float 
     out[i] = __float2bfloat16_rn(g[i] * scale);
 }
 
+__global__ void scale_kernel(float* g, long long n, float scale) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    g[i] *= scale;
+}
+
 __global__ void adamw_kernel(float* __restrict__ p, bf16* __restrict__ p16, float* __restrict__ m,
                              float* __restrict__ v, const bf16* __restrict__ g16,
                              const float* __restrict__ g32, long long n, float gscale, float lr,
@@ -500,6 +506,9 @@ void k_ce_finish(const float* logits, int Vr, int v0, const int32_t* tok, int M,
 }
 void k_scale_cast(const float* g, bf16* out, long long n, float scale, cudaStream_t s) {
   if (n > 0) scale_cast_kernel<<<ew_grid(n, 4), 256, 0, s>>>(g, out, n, scale);
+}
+void k_scale(float* g, long long n, float scale, cudaStream_t s) {
+  if (n > 0) scale_kernel<<<ew_grid(n, 4), 256, 0, s>>>(g, n, scale);
 }
 void k_adamw(float* p, bf16* p16, float* m, float* v, const bf16* g16, const float* g32,
              long long n, float gscale, float lr, float b1, float b2, float eps, float wd,

@@ -92,6 +92,7 @@ void k_ce_finish(const float* logits, int Vr, int v0, const int32_t* tok, int M,
 
 // DP gradient prep: out = bf16(scale * g)
 void k_scale_cast(const float* g, bf16* out, long long n, float scale, cudaStream_t s);
+void k_scale(float* g, long long n, float scale, cudaStream_t s);
 // AdamW on an fp32 master shard; grad is bf16 (g16) or fp32 (g32) times gscale
 void k_adamw(float* p, bf16* p16, float* m, float* v, const bf16* g16, const float* g32,
              long long n, float gscale, float lr, float b1, float b2, float eps, float wd,
