@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""bench.py — tokens/s & MFU of one asymmetric-parallel training step executed
+from a HexiScale plan on N B200s, vs the even-split plan at equal aggregate
+compute, vs the CPU reference (BASELINE.json "metric").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--plan NAME] [--impl reference]
+
+Launch for N > 1 (one rank per GPU):
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N \
+        --master-addr 127.0.0.1 --master-port P bench.py --gpus N ...
+
+A "step" = one full training step (fwd + bwd of every micro-batch, DP sync,
+AdamW) of the plan over its global batch of synthetic tokens.  `value` is
+device-timed (CUDA events on the executor stream, max over ranks) with the
+tokens resident in HBM; `e2e` is the same step through the public C ABI
+(hexexec_step) with host token buffers copied H2D and the loss read D2H
+inside the timed region (host wall clock, max over ranks).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+CFG = os.path.join(ROOT, "configs")
+
+METRIC = "tokens/s & MFU per asym plan at 1/2/4/8 B200 vs even split + CPU ref"
+# N -> (asymmetric plan, even-split plan at equal aggregate compute)
+PLANS = {
+    1: ("llama7b_4l_1gpu", None),
+    2: ("llama7b_4l_tp31", "llama7b_4l_2_even"),
+    4: ("llama7b_4l_4_asym", "llama7b_4l_4_even"),
+    8: ("llama7b_8_asym", "llama7b_8_eq_even"),
+}
+B200_SPEC = 2250.0
+
+
+def peaks():
+    p = {"bf16_tflops": 1661.7, "bf16_tflops_sustained": 1404.0, "hbm_gbs": 6553.0,
+         "source": "fallback (MEASURED_PEAKS.json absent)"}
+    f = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(f):
+        j = json.load(open(f))
+        p.update({k: j[k] for k in ("bf16_tflops", "bf16_tflops_sustained", "hbm_gbs") if k in j})
+        p["source"] = "MEASURED_PEAKS.json"
+    return p
+
+
+def load(name):
+    idx = json.load(open(os.path.join(CFG, "index.json")))[name]
+    c = open(os.path.join(CFG, "clusters", idx["cluster"] + ".json")).read()
+    m = open(os.path.join(CFG, "models", idx["model"] + ".json")).read()
+    p = open(os.path.join(CFG, "plans", name + ".json")).read()
+    return c, m, p, idx
+
+
+def model_flops(m: dict, tokens: int) -> tuple[float, float]:
+    """(reference-convention FLOPs, exact causal Llama training FLOPs) for
+    `tokens` trained tokens.  Reference: 72*S*H^2*(1+S/6H) per token per layer
+    (cost_model.cpp:17-21, :260-265).  Exact: 3x forward GEMM flops incl. the
+    causal attention products and the LM head."""
+    from oracle import bookkeeping as bk
+    m = bk.model_defaults(m)
+    L, H, S, F, V = m["num_layers"], m["hidden_dim"], m["seq_len"], m["ffn_dim"], m["vocab_size"]
+    ref = 72.0 * S * H * H * (1 + S / (6.0 * H)) * L / S * tokens
+    fwd = L * (2 * H * (4 * H + 3 * F) + 2 * S * H) + 2 * H * V
+    return ref, 3.0 * fwd * tokens
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (rank 0)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            try:
+                sm.append(float(r[1]))
+                mx.append(float(r[2]))
+            except (ValueError, IndexError):
+                continue
+            for i, n in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower() == "active":
+                    reasons.add(n)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def gather_max(vals: list, rank: int, world: int, tag: str) -> list:
+    """Max over ranks of a list of floats (TCPStore)."""
+    if world == 1:
+        return vals
+    from paper_2409_01143_b200 import dist
+    st = dist.store(rank, world)
+    st.set(f"bench/{tag}/{rank}", json.dumps(vals))
+    allv = [json.loads(st.get(f"bench/{tag}/{r}")) for r in range(world)]
+    return [max(v[i] for v in allv) for i in range(len(vals))]
+
+
+def gather_sum(vals: list, rank: int, world: int, tag: str) -> list:
+    if world == 1:
+        return vals
+    from paper_2409_01143_b200 import dist
+    st = dist.store(rank, world)
+    st.set(f"bench/{tag}/{rank}", json.dumps(vals))
+    allv = [json.loads(st.get(f"bench/{tag}/{r}")) for r in range(world)]
+    return [sum(v[i] for v in allv) for i in range(len(vals))]
+
+
+def run_plan(name: str, steps: int, warmup: int, rank: int, world: int, clocks: bool):
+    from paper_2409_01143_b200 import dist
+    c, m, p, idx = load(name)
+    ex = dist.make_executor(c, m, p, {"profile_gemm": True}, tag=f"uid-{name}")
+    role = ex.role
+    for _ in range(warmup):
+        ex.step_async()
+    ex.sync()
+    # ---- device-timed region (tokens resident in HBM)
+    dist.barrier(rank, world, f"t0-{name}")
+    ck = Clocks() if clocks else None
+    if ck:
+        ck.start()
+    ex.timer_start()
+    for _ in range(steps):
+        ex.step_async()
+    dev_ms = ex.timer_stop()
+    clk = ck.stop() if ck else None
+    st = ex.stats()
+    dev_ms = gather_max([dev_ms], rank, world, f"dev-{name}")[0]
+    # ---- e2e region: public API with host token buffers (H2D) + loss (D2H)
+    toks = [ex.synth_tokens(warmup + steps + s) if role["active"] else None for s in range(steps)]
+    dist.barrier(rank, world, f"e0-{name}")
+    t0 = time.perf_counter()
+    loss = None
+    for s in range(steps):
+        loss = ex.step(toks[s])
+    e2e_ms = (time.perf_counter() - t0) * 1e3
+    e2e_ms = gather_max([e2e_ms], rank, world, f"e2e-{name}")[0]
+    h2d = toks[0].nbytes if (role["active"] and toks[0] is not None) else 0
+    gp = st.get("gemm_profile", {})
+    lin = gp.get("tp_linear", {})
+    sums = gather_sum([float(h2d), 4.0, float(st.get("launches_last_step", 0)),
+                       float(lin.get("flops", 0.0)), float(lin.get("ms", 0.0)),
+                       float(lin.get("launches", 0)),
+                       float(st["sm_applied"]) / max(float(st["sm_total"]), 1.0)
+                       if role["active"] else 0.0],
+                      rank, world, f"sum-{name}")
+    ex.close()
+    return dict(name=name, idx=idx, cluster=json.loads(c), model=json.loads(m),
+                plan=json.loads(p), dev_ms=dev_ms, e2e_ms=e2e_ms, loss=loss, clocks=clk,
+                stats=st, h2d=sums[0], d2h=sums[1], launches=sums[2], lin_flops=sums[3],
+                lin_ms=sums[4], lin_launches=sums[5], sm_share=sums[6])
+
+
+def summarize(r: dict, steps: int, pk: dict) -> dict:
+    gb = r["plan"]["global_batch"]
+    S = r["model"]["seq_len"]
+    tokens = gb * S
+    tps = tokens * steps / (r["dev_ms"] / 1e3)
+    e2e = tokens * steps / (r["e2e_ms"] / 1e3)
+    ref_f, exact_f = model_flops(r["model"], tokens)
+    step_s = r["dev_ms"] / 1e3 / steps
+    # aggregate peak of the emulated tiers: sum over ranks of applied SM share x measured peak
+    agg = r["sm_share"] * pk["bf16_tflops"] * 1e12
+    return {"plan": r["name"], "tokens_per_s": tps, "e2e_tokens_per_s": e2e,
+            "ms_per_step": r["dev_ms"] / steps, "e2e_ms_per_step": r["e2e_ms"] / steps,
+            "mfu_ref_convention": ref_f / step_s / agg if agg else None,
+            "mfu_exact": exact_f / step_s / agg if agg else None,
+            "aggregate_sm_share": r["sm_share"], "loss": r["loss"]}
+
+
+def reference_cost(name: str, seconds: float | None):
+    """Predicted step time / MFU of the plan by the compiled reference cost
+    model (oracle/_ref), when available; null for plans it cannot price."""
+    try:
+        from oracle import refshim
+        if not refshim.available():
+            return None
+        c, m, p, _ = load(name)
+        res = refshim.check_plan(c, m, p)
+        if "cost" not in res:
+            return {"error": res.get("cost_error") or res.get("validate")}
+        out = {"predicted_s": res["cost"]["total"], "predicted_mfu": res["cost"]["mfu"]}
+        if seconds:
+            out["measured_s"] = seconds
+        return out
+    except Exception as e:  # noqa: BLE001
+        return {"error": str(e)}
+
+
+def cpu_reference(name: str, samples: int, warmup: int) -> dict:
+    """The CPU reference of this path: the fp32 numpy oracle port (the
+    reference repo has no numeric training step), on a bounded
+    sample: one sample (seq_len tokens) through a 1-layer model of the same
+    shape (embedding, 1 decoder layer, final norm, LM head, CE, backward),
+    extrapolated to the full model by the training-FLOP ratio."""
+    import numpy as np
+    from oracle import bookkeeping as bk
+    from oracle import numeric as O
+    c, m, p, _ = load(name)
+    md = bk.model_defaults(json.loads(m))
+    one = dict(md, num_layers=1)
+    cl = {"machines": {"box": {"intra_bandwidth_gbps": 900, "intra_latency_us": 3}},
+          "devices": [{"id": "cpu", "machine": "box", "memory_gib": 64, "peak_tflops": 1}],
+          "inter": {"bandwidth_gbps": 900, "latency_us": 3}}
+    plan = {"global_batch": 1, "pipelines": [{"batch": 1, "micro_batch": 1, "stages": [
+        {"devices": ["cpu"], "tp": 1, "layer_start": 0, "layer_count": 1}]}]}
+    st = O.Step(cl, one, json.dumps(plan))
+    stages = st.stage_parts(0)
+    S = md["seq_len"]
+    times = []
+    for i in range(warmup + samples):
+        G = {k: np.zeros_like(v) for k, v in st.W.items()}
+        tok = st.tokens(i, 0, 1)
+        t0 = time.perf_counter()
+        st.micro_batch(tok, stages, S, G)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+    _, f1 = model_flops(one, S)
+    _, ff = model_flops(md, S)
+    t_full = statistics.median(times) * ff / f1
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    return {"value": S / t_full, "unit": "tokens/s", "cores": cores, "kind": "port",
+            "sample": (f"numpy fp32 oracle (oracle/numeric.py), 1 sample x {S} tokens through "
+                       f"embedding + 1 decoder layer + LM head/CE, fwd+bwd, median of {samples}, "
+                       f"x{ff / f1:.2f} training-FLOP ratio to the {md['num_layers']}-layer model; "
+                       "BLAS threads = all host cores"),
+            "sample_s": statistics.median(times)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--plan", default=None, help="configs/plans/<name>.json (asymmetric arm)")
+    ap.add_argument("--even", default=None, help="even-split comparison plan ('none' to skip)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    a = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != a.gpus and "RANK" in os.environ:
+        raise SystemExit(f"WORLD_SIZE {world} != --gpus {a.gpus}")
+    asym, even = PLANS.get(a.gpus, (None, None))
+    if a.plan:
+        asym = a.plan
+        even = None
+    if a.even:
+        even = None if a.even == "none" else a.even
+    if asym is None:
+        raise SystemExit(f"no default plan for {a.gpus} GPUs; pass --plan")
+    _, m_doc, _, _ = load(asym)
+    model = json.loads(m_doc)
+    config = {"workload": f"{asym}: {INDEX_DESC.get(asym, asym)}", "plan": asym,
+              "model": model, "global_batch": json.loads(load(asym)[2])["global_batch"],
+              "seq_len": model["seq_len"], "even_split_plan": even,
+              "l2": "working set per step >> 126 MB L2 (weights + optimizer state + activations)",
+              "parallelism": "plan-defined asymmetric DP/PP/TP, one process per GPU"}
+
+    if a.impl == "reference":
+        if rank != 0:
+            return
+        ref = cpu_reference(asym, samples=max(1, a.steps), warmup=min(a.warmup, 1))
+        line = {"metric": METRIC, "value": ref["value"], "unit": "tokens/s", "impl": "reference",
+                "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+                "ms_per_step": json.loads(load(asym)[2])["global_batch"] * model["seq_len"]
+                / ref["value"] * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic", "config": config,
+                "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": ref["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0},
+                "reference_cost_model": reference_cost(asym, None)}
+        print(json.dumps(line), flush=True)
+        return
+
+    pk = peaks()
+    r = run_plan(asym, a.steps, a.warmup, rank, world, clocks=(rank == 0))
+    s = summarize(r, a.steps, pk)
+    ev = None
+    if even:
+        re_ = run_plan(even, a.steps, a.warmup, rank, world, clocks=False)
+        ev = summarize(re_, a.steps, pk)
+    if rank != 0:
+        return
+    lin_ms_launch = r["lin_ms"] / max(r["lin_launches"], 1)
+    lin_flops_launch = r["lin_flops"] / max(r["lin_launches"], 1)
+    achieved = lin_flops_launch / (lin_ms_launch / 1e3) / 1e12 if lin_ms_launch > 0 else None
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tf):
+        traffic = json.load(open(tf)).get("bytes_per_launch")
+    cpu = None
+    if a.gpus == 1 and not a.no_cpu_baseline:
+        cb = cpu_reference(asym, samples=1, warmup=0)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    line = {
+        "metric": METRIC, "value": s["tokens_per_s"], "unit": "tokens/s", "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": s["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic tokens (counter RNG), random-init weights (N(0,0.02) Irwin-Hall)",
+        "config": config,
+        "mfu": {"ref_convention": s["mfu_ref_convention"], "exact": s["mfu_exact"],
+                "peak_per_rank": f"sm_share x {pk['bf16_tflops']} TFLOPS ({pk['source']})",
+                "aggregate_sm_share": s["aggregate_sm_share"]},
+        "even_split": ev,
+        "mfu_gap_vs_even": (ev["mfu_ref_convention"] - s["mfu_ref_convention"]) if ev else None,
+        "e2e": {"value": s["e2e_tokens_per_s"], "unit": "tokens/s",
+                "h2d_bytes_per_step": int(r["h2d"]), "d2h_bytes_per_step": int(r["d2h"])},
+        "gpu_launches": int(r["launches"] * a.steps),
+        "roofline": {"bound": "tensor", "kernel": "tcgen05 TP GEMMs (QKV/O/gate-up/down, fwd+dgrad+wgrad)",
+                     "achieved": achieved, "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                     "frac": achieved / pk["bf16_tflops_sustained"] if achieved else None,
+                     "peak_kind": "sustained (kernel timed inside a long step)",
+                     "launches_per_step": r["lin_launches"],
+                     "algorithmic_flops_per_launch": lin_flops_launch,
+                     "avg_launch_ms": lin_ms_launch, "traffic": traffic},
+        "gemm_profile_rank0": r["stats"].get("gemm_profile"),
+        "phase_ms_rank0": r["stats"].get("ms"),
+        "sm_cap_rank0": {k: r["stats"].get(k) for k in ("sm_cap_mode", "sm_applied", "sm_total")},
+        "clocks": r["clocks"],
+        "cpu_baseline": cpu,
+        "reference_cost_model": reference_cost(asym, s["ms_per_step"] / 1e3),
+        "loss": s["loss"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+INDEX_DESC = {
+    "llama7b_4l_1gpu": "Llama-7B-shaped 4-layer block, seq 2048, global batch 8, one B200 (tp=1)",
+    "llama7b_4l_tp31": "Llama-7B-shaped 4-layer block, seq 2048, TP=2 widths 3:1 on 2xB200, "
+                       "rank 1 SM-capped to 1/3",
+    "llama7b_4l_4_asym": "Llama-7B-shaped 4-layer block, hexplan_schedule plan on 4xB200 "
+                         "tiers [F,F,1/2,1/2]",
+    "llama7b_8_asym": "Llama-7B (32 layers) on 8xB200 tiers [F,F,F,F,1/2,1/2,1/3,1/3]: "
+                      "hexplan_schedule plan, asymmetric DP 15/12/12/12/13",
+    "llama13b_pp3_asymtp": "Llama-13B 3-stage pipeline 16/14/10, asymmetric TP inside stages",
+    "llama30b_8_tiers": "Llama-30B layers under a full hexplan_schedule plan, 8xB200 SM-capped tiers",
+}
+
+if __name__ == "__main__":
+    main()

@@ -40,6 +40,11 @@ CLUSTERS = {
     "b200_8_tiers": cluster(TIERS8, {"tierF": ["g0", "g1", "g2", "g3"], "tierH": ["g4", "g5"],
                                      "tierT": ["g6", "g7"]}),
     "b200_8_even": cluster([(f"g{i}", F) for i in range(8)]),
+    # homogeneous clusters with the SAME aggregate compute as the capped ones
+    # (the "even-split plan at equal aggregate compute" comparison)
+    "b200_2_eq": cluster([(f"g{i}", (F + THIRD) / 2) for i in range(2)]),
+    "b200_4_eq": cluster([(f"g{i}", (2 * F + 2 * HALF) / 4) for i in range(4)]),
+    "b200_8_eq": cluster([(f"g{i}", (4 * F + 2 * HALF + 2 * THIRD) / 8) for i in range(8)]),
 }
 
 MODELS = {
@@ -121,6 +126,16 @@ PLANNED = {
                            "state_multiplier": 2.5}),
     "llama7b_4l_2_asym": ("b200_2_capped", "llama7b_4l", "schedule",
                           {"global_batch": 8, "iterations": 20, "seed": 0, "threads": 8,
+                           "state_multiplier": 2.5}),
+    # even-split plans (hexplan_symmetric_baseline) at equal aggregate compute
+    "llama7b_4l_2_even": ("b200_2_eq", "llama7b_4l", "symmetric",
+                          {"global_batch": 8, "iterations": 20, "seed": 0, "threads": 8,
+                           "state_multiplier": 2.5}),
+    "llama7b_4l_4_even": ("b200_4_eq", "llama7b_4l", "symmetric",
+                          {"global_batch": 16, "iterations": 30, "seed": 0, "threads": 8,
+                           "state_multiplier": 2.5}),
+    "llama7b_8_eq_even": ("b200_8_eq", "llama7b", "symmetric",
+                          {"global_batch": 64, "iterations": 50, "seed": 0, "threads": 8,
                            "state_multiplier": 2.5}),
 }
 

@@ -189,6 +189,15 @@ hexexec_status hexexec_sync(hexexec_ctx* ctx, char* err, size_t err_len) {
   return guarded(err, err_len, [&] { hexexec::executor_sync(*ctx->ex); });
 }
 
+hexexec_status hexexec_timer(hexexec_ctx* ctx, int stop, float* ms_out, char* err,
+                             size_t err_len) {
+  if (!ctx || !ctx->ex || (stop && !ms_out)) {
+    set_err(err, err_len, "null argument");
+    return HEXEXEC_ERR_INVALID;
+  }
+  return guarded(err, err_len, [&] { hexexec::executor_timer(*ctx->ex, stop, ms_out); });
+}
+
 hexexec_status hexexec_last_loss(hexexec_ctx* ctx, float* loss_out, char* err, size_t err_len) {
   if (!ctx || !ctx->ex || !loss_out) {
     set_err(err, err_len, "null argument");

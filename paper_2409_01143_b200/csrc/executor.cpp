@@ -68,6 +68,7 @@ ExecConfig parse_exec_config(const std::string& text) {
       else if (k == "sm_cap") c.sm_cap = v.get<std::string>();
       else if (k == "dp_comm_dtype") c.dp_comm_dtype = v.get<std::string>();
       else if (k == "validate_only") c.validate_only = v.get<bool>();
+      else if (k == "profile_gemm") c.profile_gemm = v.get<bool>();
       else throw ParseError("exec config: unknown key '" + k + "'");
     } catch (const nlohmann::json::exception& e) {
       throw ParseError("exec config: bad value for '" + k + "'");
@@ -184,6 +185,7 @@ class Executor {
   int64_t step_index = 0;
   // stats
   cudaEvent_t ev[6] = {};
+  cudaEvent_t tmr_[2] = {};
   float phase_ms[5] = {0, 0, 0, 0, 0};
   int64_t launches_step = 0, launches_total = 0;
   int64_t nccl_calls_step = 0;
@@ -206,6 +208,13 @@ class Executor {
     loss_host = nullptr;
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    for (auto& e : tmr_)
+      if (e) cudaEventDestroy(e);
+    for (auto& r : gemm_pool_) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    gemm_pool_.clear();
     if (own_stream && stream) cudaStreamDestroy(stream);
     stream = nullptr;
   }
@@ -247,6 +256,7 @@ class Executor {
     HX_CUDA(cudaDeviceGetAttribute(&sm_total, cudaDevAttrMultiProcessorCount, dev));
     setup_stream();
     for (auto& e : ev) HX_CUDA(cudaEventCreate(&e));
+    for (auto& e : tmr_) HX_CUDA(cudaEventCreate(&e));
     setup_comms(uid, uid_len);
     if (role.active) {
       allocate();
@@ -489,10 +499,53 @@ class Executor {
     if (e != cudaSuccess) throw CudaError(std::string("kernel launch: ") + cudaGetErrorString(e));
   }
 
+  // GEMM launch; with profile_gemm, each launch is bracketed by CUDA events on
+  // the executor stream and its algorithmic FLOPs recorded (kind: 0 = TP
+  // linear layer, 1 = attention product, 2 = LM head)
+  int gemm_kind_ = 0;
+  struct GemmRec {
+    cudaEvent_t a, b;
+    double flops;
+    int kind;
+  };
+  std::vector<GemmRec> gemm_pool_;
+  size_t gemm_used_ = 0;
+  double gemm_ms_[3] = {0, 0, 0}, gemm_flops_[3] = {0, 0, 0};
+  int64_t gemm_count_[3] = {0, 0, 0};
+
   void gemm(const GemmDesc& g) {
+    GemmRec* rec = nullptr;
+    if (cfg.profile_gemm) {
+      if (gemm_used_ == gemm_pool_.size()) {
+        GemmRec r{};
+        HX_CUDA(cudaEventCreate(&r.a));
+        HX_CUDA(cudaEventCreate(&r.b));
+        gemm_pool_.push_back(r);
+      }
+      rec = &gemm_pool_[gemm_used_++];
+      double full = 2.0 * g.M * double(g.N) * g.K * g.nb1 * g.nb2;
+      rec->flops = g.causal != kCausalNone ? full * (double(g.M) + 1) / (2.0 * g.M) : full;
+      rec->kind = gemm_kind_;
+      HX_CUDA(cudaEventRecord(rec->a, stream));
+    }
     cudaError_t e = gemm_bf16(g, stream);
     if (e != cudaSuccess) throw CudaError(std::string("gemm: ") + cudaGetErrorString(e));
+    if (rec) HX_CUDA(cudaEventRecord(rec->b, stream));
     ++launches_step;
+  }
+
+  int64_t steps_since_collect_ = 0;
+  void collect_gemm_profile() {
+    for (int k = 0; k < 3; ++k) gemm_ms_[k] = gemm_flops_[k] = 0, gemm_count_[k] = 0;
+    for (size_t i = 0; i < gemm_used_; ++i) {
+      float ms = 0;
+      if (cudaEventElapsedTime(&ms, gemm_pool_[i].a, gemm_pool_[i].b) == cudaSuccess) {
+        gemm_ms_[gemm_pool_[i].kind] += ms;
+        gemm_flops_[gemm_pool_[i].kind] += gemm_pool_[i].flops;
+        gemm_count_[gemm_pool_[i].kind] += 1;
+      }
+    }
+    gemm_used_ = 0;
   }
 
   // plain 2D GEMM helper
@@ -574,6 +627,7 @@ class Executor {
   // per (sample b, head h): scores = q k^T / sqrt(d) (causal tiles), P = softmax,
   // attn = P v -- batched over z = h + nh * b straight out of the QKV buffer
   void attention_fwd(LayerActs& a) {
+    gemm_kind_ = 1;
     const int64_t SS2 = S * S;
     GemmDesc g;
     g.M = int(S);
@@ -607,13 +661,16 @@ class Executor {
     o.cbs2 = S * kr;
     o.causal = kCausalKLower;
     gemm(o);
+    gemm_kind_ = 0;
   }
 
   void head_fwd(Slot& sl, int64_t mbi) {
     const float eps = float(L.model.norm_eps);
     k_rmsnorm_fwd(sl.x[size_t(nl)], nullptr, nullptr, final_norm.p32, sl.xf, sl.rstdf, int(M), int(H), eps, stream);
     kcheck();
+    gemm_kind_ = 2;
     gemm(g2(M, Vr, H, sl.xf, 0, H, lm_head.p16, 0, H, logits, Vr, 1));
+    gemm_kind_ = 0;
     float* lmax = ce_scr;
     float* lsum = ce_scr + M;
     float* st2 = ce_scr + 2 * M;
@@ -696,6 +753,7 @@ class Executor {
   }
 
   void attention_bwd(LayerActs& a) {
+    gemm_kind_ = 1;
     const int64_t SS2 = S * S;
     // dP = dO V^T
     GemmDesc g;
@@ -744,6 +802,7 @@ class Executor {
     v.C = dqkv + 2 * d;
     v.causal = kCausalKUpper;
     gemm(v);
+    gemm_kind_ = 0;
   }
 
   // backward of one micro-batch; dx_top (fp32) is the grad of the stage output
@@ -753,10 +812,12 @@ class Executor {
     float* nxt = dx[1];
     bf16* curb = dxb;
     if (role.last_stage) {
+      gemm_kind_ = 2;
       gemm(g2(M, H, Vr, sl.dlogits, 0, Vr, lm_head.p16, 1, H, dy16, H, 0));
       GemmDesc g = g2(Vr, H, M, sl.dlogits, 1, Vr, sl.xf, 1, H, lm_head.g32, H, 1);
       g.beta = accum_first_ ? 0 : 1;
       gemm(g);
+      gemm_kind_ = 0;
       tp_allreduce_bf16(dy16, M * H);
       k_rmsnorm_bwd(dy16, nullptr, sl.x[size_t(nl)], sl.rstdf, final_norm.p32, nullptr, cur, curb,
                     final_norm.g32, int(M), int(H), stream);
@@ -975,6 +1036,8 @@ class Executor {
     HX_CUDA(cudaStreamSynchronize(stream));
     last_loss = loss_host[0] / float(L.plan.global_batch * S);
     if (role.active) collect_times();
+    steps_since_collect_ = 1;
+    collect_gemm_profile();
     if (loss_out) *loss_out = last_loss;
   }
 
@@ -1005,6 +1068,16 @@ class Executor {
     j["ms"] = {{"prologue", phase_ms[0]}, {"pipeline", phase_ms[1]}, {"dp_sync", phase_ms[2]},
                {"optimizer", phase_ms[3]}, {"step", phase_ms[4]}};
     j["last_loss"] = last_loss;
+    if (cfg.profile_gemm) {
+      const char* names[3] = {"tp_linear", "attention", "lm_head"};
+      ojson g;
+      for (int k = 0; k < 3; ++k)
+        g[names[k]] = {{"launches", gemm_count_[k]}, {"ms", gemm_ms_[k]},
+                       {"flops", gemm_flops_[k]},
+                       {"tflops", gemm_ms_[k] > 0 ? gemm_flops_[k] / gemm_ms_[k] / 1e9 : 0.0}};
+      g["steps"] = steps_since_collect_;
+      j["gemm_profile"] = g;
+    }
     return j.dump();
   }
 };
@@ -1027,7 +1100,19 @@ void executor_step(Executor& e, const int32_t* t, size_t n, float* loss) { e.ste
 
 void executor_step_async(Executor& e) {
   e.tokens_from_host_ = nullptr;
+  if (e.gemm_used_ == 0) e.steps_since_collect_ = 0;
   e.step_enqueue();
+  ++e.steps_since_collect_;
+}
+
+void executor_timer(Executor& e, int stop, float* ms) {
+  if (!stop) {
+    HX_CUDA(cudaEventRecord(e.tmr_[0], e.stream));
+    return;
+  }
+  HX_CUDA(cudaEventRecord(e.tmr_[1], e.stream));
+  HX_CUDA(cudaEventSynchronize(e.tmr_[1]));
+  HX_CUDA(cudaEventElapsedTime(ms, e.tmr_[0], e.tmr_[1]));
 }
 
 void executor_sync(Executor& e) {
@@ -1035,6 +1120,7 @@ void executor_sync(Executor& e) {
   HX_CUDA(cudaMemcpy(e.loss_host, e.loss_acc, 4, cudaMemcpyDeviceToHost));
   e.last_loss = e.loss_host[0] / float(e.L.plan.global_batch * e.S);
   if (e.role.active) e.collect_times();
+  e.collect_gemm_profile();
 }
 
 float executor_last_loss(Executor& e) { return e.last_loss; }

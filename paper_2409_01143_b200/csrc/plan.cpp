@@ -421,12 +421,15 @@ Layout build_layout(const std::string& cluster_json, const std::string& model_js
 
   L.tensors = make_catalogue(m);
   L.roles.assign(size_t(n), RankRole{});
-  const double maxp = c.max_peak();
+  // emulated tier: the device's share of a full B200 (2250 TFLOPS dense BF16,
+  // the c_d the probe clusters use), capped at 1
+  constexpr double kB200Peak = 2250.0;
   for (int r = 0; r < n; ++r) {
     RankRole& role = L.roles[size_t(r)];
     role.device = L.device_of_rank[size_t(r)];
     const Device& dv = c.devices[size_t(role.device)];
-    role.sm_fraction = dv.sm_fraction > 0 ? dv.sm_fraction : (maxp > 0 ? dv.peak_tflops / maxp : 1.0);
+    role.sm_fraction =
+        dv.sm_fraction > 0 ? dv.sm_fraction : std::min(1.0, dv.peak_tflops / kB200Peak);
     role.sm_count = dv.sm_count;
   }
 

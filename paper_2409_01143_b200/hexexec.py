@@ -100,6 +100,16 @@ class Executor:
         err = L.errbuf()
         L.check(L.hexexec_sync(self._h, err, len(err)), err)
 
+    def timer_start(self):
+        err = L.errbuf()
+        L.check(L.hexexec_timer(self._h, 0, None, err, len(err)), err)
+
+    def timer_stop(self) -> float:
+        ms = C.c_float(0.0)
+        err = L.errbuf()
+        L.check(L.hexexec_timer(self._h, 1, C.byref(ms), err, len(err)), err)
+        return float(ms.value)
+
     def last_loss(self) -> float:
         loss = C.c_float(0.0)
         err = L.errbuf()
