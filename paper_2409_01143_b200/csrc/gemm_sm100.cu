@@ -229,19 +229,29 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float* res = p.R ? p.R + cbase + col : nullptr;
           if (full_chunk && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
             float4* o4 = reinterpret_cast<float4*>(out);
+            // issue every load of the chunk before the first store (no aliasing
+            // stalls: 8 independent 16-byte loads in flight per thread)
+            if (p.beta || res) {
+              float4 o[8];
+              const float4* src = p.beta ? o4 : reinterpret_cast<const float4*>(res);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              float4 w = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-              if (p.beta) {
-                float4 o = o4[i];
-                w.x += o.x; w.y += o.y; w.z += o.z; w.w += o.w;
+              for (int i = 0; i < 8; ++i) o[i] = __ldcs(src + i);
+              if (p.beta && res) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  float4 q = __ldcs(reinterpret_cast<const float4*>(res) + i);
+                  o[i].x += q.x; o[i].y += q.y; o[i].z += q.z; o[i].w += q.w;
+                }
               }
-              if (res) {
-                float4 o = reinterpret_cast<const float4*>(res)[i];
-                w.x += o.x; w.y += o.y; w.z += o.z; w.w += o.w;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                v[4 * i] += o[i].x; v[4 * i + 1] += o[i].y;
+                v[4 * i + 2] += o[i].z; v[4 * i + 3] += o[i].w;
               }
-              o4[i] = w;
             }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              o4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
           } else {
             for (int i = 0; i < 32 && col + i < p.N; ++i)
               out[i] = (p.beta ? out[i] : 0.f) + (res ? res[i] : 0.f) + v[i];
