@@ -132,79 +132,89 @@ __global__ void residual_add_kernel(const float* x, const bf16* y, float* xo, lo
     xo[i] = x[i] + bf(y[i]);
 }
 
-// dx = dres + r * (dy*g - xhat * mean(dy*g*xhat)),  xhat = x*r;  dg += dy*xhat
+// RMSNorm backward, two passes:
+//   (1) warp per row: c[m] = r^3/H * sum_j dy*g*x
+//   (2) column tiles (coalesced float4 columns x 64-row bands):
+//       dx = dres + r*dy*g - x*c ;  dg[j] += sum_rows dy*x*r  (register
+//       accumulation over the band, one atomic per column per band)
 template <bool kDyBf16>
-__global__ void rmsnorm_bwd_kernel(const bf16* __restrict__ dyb, const float* __restrict__ dyf,
-                                   const float* __restrict__ x, const float* __restrict__ rstd,
-                                   const float* __restrict__ g, const float* __restrict__ dres,
-                                   float* __restrict__ dx, bf16* __restrict__ dxb,
-                                   float* __restrict__ dg, int M, int H, int rows_per_warp) {
-  extern __shared__ float sdg[];  // [H] per block partial dg
-  const int warps = blockDim.x / 32;
-  const int wid = threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  for (int i = threadIdx.x; i < H; i += blockDim.x) sdg[i] = 0.f;
-  __syncthreads();
-  int row0 = (blockIdx.x * warps + wid) * rows_per_warp;
-  for (int rr = 0; rr < rows_per_warp; ++rr) {
-    int row = row0 + rr;
-    if (row >= M) break;
+__device__ __forceinline__ float4 load_dy(const bf16* dyb, const float* dyf, long long off) {
+  if (kDyBf16) {
+    uint2 w = *reinterpret_cast<const uint2*>(dyb + off);
+    __nv_bfloat162 a = *reinterpret_cast<__nv_bfloat162*>(&w.x);
+    __nv_bfloat162 b = *reinterpret_cast<__nv_bfloat162*>(&w.y);
+    return make_float4(__low2float(a), __high2float(a), __low2float(b), __high2float(b));
+  }
+  return *reinterpret_cast<const float4*>(dyf + off);
+}
+
+template <bool kDyBf16>
+__global__ void rmsnorm_bwd_dot_kernel(const bf16* __restrict__ dyb, const float* __restrict__ dyf,
+                                       const float* __restrict__ x, const float* __restrict__ rstd,
+                                       const float* __restrict__ g, float* __restrict__ coef,
+                                       int M, int H) {
+  int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  int lane = threadIdx.x % 32;
+  if (row >= M) return;
+  const long long base = (long long)row * H;
+  float dot = 0.f;
+  for (int i = lane * 4; i < H; i += 128) {
+    float4 xv = *reinterpret_cast<const float4*>(x + base + i);
+    float4 gv = *reinterpret_cast<const float4*>(g + i);
+    float4 d = load_dy<kDyBf16>(dyb, dyf, base + i);
+    dot += d.x * gv.x * xv.x + d.y * gv.y * xv.y + d.z * gv.z * xv.z + d.w * gv.w * xv.w;
+  }
+  dot = warp_sum(dot);
+  if (lane == 0) {
     const float r = rstd[row];
-    const float* xr = x + (long long)row * H;
-    float dot = 0.f;
-    for (int i = lane * 4; i < H; i += 128) {
-      float4 xv = *reinterpret_cast<const float4*>(xr + i);
-      float4 gv = *reinterpret_cast<const float4*>(g + i);
-      float d0, d1, d2, d3;
-      if (kDyBf16) {
-        uint2 w = *reinterpret_cast<const uint2*>(dyb + (long long)row * H + i);
-        __nv_bfloat162 a = *reinterpret_cast<__nv_bfloat162*>(&w.x);
-        __nv_bfloat162 b = *reinterpret_cast<__nv_bfloat162*>(&w.y);
-        d0 = __low2float(a); d1 = __high2float(a); d2 = __low2float(b); d3 = __high2float(b);
-      } else {
-        float4 dv = *reinterpret_cast<const float4*>(dyf + (long long)row * H + i);
-        d0 = dv.x; d1 = dv.y; d2 = dv.z; d3 = dv.w;
-      }
-      dot += d0 * gv.x * xv.x + d1 * gv.y * xv.y + d2 * gv.z * xv.z + d3 * gv.w * xv.w;
-      atomicAdd(&sdg[i + 0], d0 * xv.x * r);
-      atomicAdd(&sdg[i + 1], d1 * xv.y * r);
-      atomicAdd(&sdg[i + 2], d2 * xv.z * r);
-      atomicAdd(&sdg[i + 3], d3 * xv.w * r);
+    coef[row] = dot * r * r * r / float(H);
+  }
+}
+
+template <bool kDyBf16>
+__global__ void rmsnorm_bwd_dx_kernel(const bf16* __restrict__ dyb, const float* __restrict__ dyf,
+                                      const float* __restrict__ x, const float* __restrict__ rstd,
+                                      const float* __restrict__ coef,
+                                      const float* __restrict__ g, const float* __restrict__ dres,
+                                      float* __restrict__ dx, bf16* __restrict__ dxb,
+                                      float* __restrict__ dg, int M, int H, int band) {
+  const int col = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (col >= H) return;
+  const int r0 = blockIdx.y * band;
+  const int r1 = min(M, r0 + band);
+  const float4 gv = *reinterpret_cast<const float4*>(g + col);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int row = r0; row < r1; ++row) {
+    const long long off = (long long)row * H + col;
+    const float r = rstd[row];
+    const float c = coef[row];
+    float4 xv = *reinterpret_cast<const float4*>(x + off);
+    float4 d = load_dy<kDyBf16>(dyb, dyf, off);
+    acc.x += d.x * xv.x * r;
+    acc.y += d.y * xv.y * r;
+    acc.z += d.z * xv.z * r;
+    acc.w += d.w * xv.w * r;
+    float4 o;
+    o.x = r * d.x * gv.x - xv.x * c;
+    o.y = r * d.y * gv.y - xv.y * c;
+    o.z = r * d.z * gv.z - xv.z * c;
+    o.w = r * d.w * gv.w - xv.w * c;
+    if (dres) {
+      float4 rv = *reinterpret_cast<const float4*>(dres + off);
+      o.x += rv.x; o.y += rv.y; o.z += rv.z; o.w += rv.w;
     }
-    dot = warp_sum(dot) * r * r * r / float(H);
-    for (int i = lane * 4; i < H; i += 128) {
-      float4 xv = *reinterpret_cast<const float4*>(xr + i);
-      float4 gv = *reinterpret_cast<const float4*>(g + i);
-      float d[4];
-      if (kDyBf16) {
-        uint2 w = *reinterpret_cast<const uint2*>(dyb + (long long)row * H + i);
-        __nv_bfloat162 a = *reinterpret_cast<__nv_bfloat162*>(&w.x);
-        __nv_bfloat162 b = *reinterpret_cast<__nv_bfloat162*>(&w.y);
-        d[0] = __low2float(a); d[1] = __high2float(a); d[2] = __low2float(b); d[3] = __high2float(b);
-      } else {
-        float4 dv = *reinterpret_cast<const float4*>(dyf + (long long)row * H + i);
-        d[0] = dv.x; d[1] = dv.y; d[2] = dv.z; d[3] = dv.w;
-      }
-      float4 o;
-      o.x = r * (d[0] * gv.x) - xv.x * dot;
-      o.y = r * (d[1] * gv.y) - xv.y * dot;
-      o.z = r * (d[2] * gv.z) - xv.z * dot;
-      o.w = r * (d[3] * gv.w) - xv.w * dot;
-      if (dres) {
-        float4 rv = *reinterpret_cast<const float4*>(dres + (long long)row * H + i);
-        o.x += rv.x; o.y += rv.y; o.z += rv.z; o.w += rv.w;
-      }
-      *reinterpret_cast<float4*>(dx + (long long)row * H + i) = o;
-      if (dxb) {
-        uint2 w;
-        w.x = pack_bf16x2(o.x, o.y);
-        w.y = pack_bf16x2(o.z, o.w);
-        *reinterpret_cast<uint2*>(dxb + (long long)row * H + i) = w;
-      }
+    *reinterpret_cast<float4*>(dx + off) = o;
+    if (dxb) {
+      uint2 w;
+      w.x = pack_bf16x2(o.x, o.y);
+      w.y = pack_bf16x2(o.z, o.w);
+      *reinterpret_cast<uint2*>(dxb + off) = w;
     }
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < H; i += blockDim.x) atomicAdd(&dg[i], sdg[i]);
+  atomicAdd(dg + col + 0, acc.x);
+  atomicAdd(dg + col + 1, acc.y);
+  atomicAdd(dg + col + 2, acc.z);
+  atomicAdd(dg + col + 3, acc.w);
 }
 
 // ------------------------------------------------------------------ rope
@@ -408,17 +418,53 @@ __global__ void adamw_kernel(float* __restrict__ p, bf16* __restrict__ p16, floa
                              float* __restrict__ v, const bf16* __restrict__ g16,
                              const float* __restrict__ g32, long long n, float gscale, float lr,
                              float b1, float b2, float eps, float wd, float bc1, float bc2) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+  // 4 elements per thread-iteration: float4 p/m/v, 8-byte bf16 grad / copy
+  const long long n4 = n / 4;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    float gg[4];
+    if (g16) {
+      uint2 w = __ldcs(reinterpret_cast<const uint2*>(g16) + i);
+      __nv_bfloat162 a = *reinterpret_cast<__nv_bfloat162*>(&w.x);
+      __nv_bfloat162 b = *reinterpret_cast<__nv_bfloat162*>(&w.y);
+      gg[0] = __low2float(a); gg[1] = __high2float(a); gg[2] = __low2float(b); gg[3] = __high2float(b);
+    } else {
+      float4 w = __ldcs(reinterpret_cast<const float4*>(g32) + i);
+      gg[0] = w.x; gg[1] = w.y; gg[2] = w.z; gg[3] = w.w;
+    }
+    float4 pm = reinterpret_cast<float4*>(p)[i];
+    float4 mm = reinterpret_cast<float4*>(m)[i];
+    float4 vv = reinterpret_cast<float4*>(v)[i];
+    float* pp = &pm.x;
+    float* mp = &mm.x;
+    float* vp = &vv.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float g = gg[k] * gscale;
+      mp[k] = b1 * mp[k] + (1.f - b1) * g;
+      vp[k] = b2 * vp[k] + (1.f - b2) * g * g;
+      pp[k] = pp[k] - lr * ((mp[k] / bc1) / (sqrtf(vp[k] / bc2) + eps) + wd * pp[k]);
+    }
+    reinterpret_cast<float4*>(p)[i] = pm;
+    reinterpret_cast<float4*>(m)[i] = mm;
+    reinterpret_cast<float4*>(v)[i] = vv;
+    if (p16) {
+      uint2 w;
+      w.x = pack_bf16x2(pm.x, pm.y);
+      w.y = pack_bf16x2(pm.z, pm.w);
+      reinterpret_cast<uint2*>(p16)[i] = w;
+    }
+  }
+  // scalar tail (n % 4)
+  for (long long i = n4 * 4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     float g = (g16 ? bf(g16[i]) : g32[i]) * gscale;
     float mi = b1 * m[i] + (1.f - b1) * g;
     float vi = b2 * v[i] + (1.f - b2) * g * g;
     m[i] = mi;
     v[i] = vi;
-    float mh = mi / bc1;
-    float vh = vi / bc2;
     float pi = p[i];
-    pi = pi - lr * (mh / (sqrtf(vh) + eps) + wd * pi);
+    pi = pi - lr * ((mi / bc1) / (sqrtf(vi / bc2) + eps) + wd * pi);
     p[i] = pi;
     if (p16) p16[i] = __float2bfloat16_rn(pi);
   }
@@ -459,15 +505,17 @@ void k_residual_add(const float* x, const bf16* y, float* xo, long long n, cudaS
 }
 void k_rmsnorm_bwd(const bf16* dyb, const float* dyf, const float* x, const float* rstd,
                    const float* g, const float* dres, float* dx, bf16* dxb, float* dg, int M,
-                   int H, cudaStream_t s) {
+                   int H, float* coef, cudaStream_t s) {
   if (M <= 0) return;
-  const int warps = 8, rpw = 4;
-  int grid = (M + warps * rpw - 1) / (warps * rpw);
-  size_t sm = size_t(H) * sizeof(float);
-  if (dyb)
-    rmsnorm_bwd_kernel<true><<<grid, warps * 32, sm, s>>>(dyb, dyf, x, rstd, g, dres, dx, dxb, dg, M, H, rpw);
-  else
-    rmsnorm_bwd_kernel<false><<<grid, warps * 32, sm, s>>>(dyb, dyf, x, rstd, g, dres, dx, dxb, dg, M, H, rpw);
+  const int band = 64;
+  dim3 g2((H / 4 + 127) / 128, (M + band - 1) / band);
+  if (dyb) {
+    rmsnorm_bwd_dot_kernel<true><<<row_grid(M, 8), 256, 0, s>>>(dyb, dyf, x, rstd, g, coef, M, H);
+    rmsnorm_bwd_dx_kernel<true><<<g2, 128, 0, s>>>(dyb, dyf, x, rstd, coef, g, dres, dx, dxb, dg, M, H, band);
+  } else {
+    rmsnorm_bwd_dot_kernel<false><<<row_grid(M, 8), 256, 0, s>>>(dyb, dyf, x, rstd, g, coef, M, H);
+    rmsnorm_bwd_dx_kernel<false><<<g2, 128, 0, s>>>(dyb, dyf, x, rstd, coef, g, dres, dx, dxb, dg, M, H, band);
+  }
 }
 void k_rope(bf16* qkv, int M, int S, int nh, int d, float theta, int inverse, cudaStream_t s) {
   long long n = (long long)M * nh * (d / 2);
