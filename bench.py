@@ -143,9 +143,9 @@ def gather_sum(vals: list, rank: int, world: int, tag: str) -> list:
 def run_plan(name: str, steps: int, warmup: int, rank: int, world: int, clocks: bool):
     from paper_2409_01143_b200 import dist
     c, m, p, idx = load(name)
-    ex = dist.make_executor(c, m, p, {"profile_gemm": True}, tag=f"uid-{name}")
+    ex = dist.make_executor(c, m, p, {}, tag=f"uid-{name}")
     role = ex.role
-    for _ in range(warmup):
+    for _ in range(warmup):      # step 0 eager, step 1 captured into the CUDA graph
         ex.step_async()
     ex.sync()
     # ---- device-timed region (tokens resident in HBM)
@@ -158,7 +158,7 @@ def run_plan(name: str, steps: int, warmup: int, rank: int, world: int, clocks: 
         ex.step_async()
     dev_ms = ex.timer_stop()
     clk = ck.stop() if ck else None
-    st = ex.stats()
+    launches_step = ex.stats().get("launches_last_step", 0)
     dev_ms = gather_max([dev_ms], rank, world, f"dev-{name}")[0]
     # ---- e2e region: public API with host token buffers (H2D) + loss (D2H)
     toks = [ex.synth_tokens(warmup + steps + s) if role["active"] else None for s in range(steps)]
@@ -170,9 +170,18 @@ def run_plan(name: str, steps: int, warmup: int, rank: int, world: int, clocks: 
     e2e_ms = (time.perf_counter() - t0) * 1e3
     e2e_ms = gather_max([e2e_ms], rank, world, f"e2e-{name}")[0]
     h2d = toks[0].nbytes if (role["active"] and toks[0] is not None) else 0
+    # ---- profiled pass (eager, CUDA events around every GEMM and after every op):
+    # roofline evidence for the TP GEMMs + per-kernel-class step timeline
+    ex.set_profile(True)
+    dist.barrier(rank, world, f"p0-{name}")
+    for _ in range(max(1, min(steps, 2))):
+        ex.step_async()
+    ex.sync()
+    st = ex.stats()
+    ex.set_profile(False)
     gp = st.get("gemm_profile", {})
     lin = gp.get("tp_linear", {})
-    sums = gather_sum([float(h2d), 4.0, float(st.get("launches_last_step", 0)),
+    sums = gather_sum([float(h2d), 4.0, float(launches_step),
                        float(lin.get("flops", 0.0)), float(lin.get("ms", 0.0)),
                        float(lin.get("launches", 0)),
                        float(st["sm_applied"]) / max(float(st["sm_total"]), 1.0)
@@ -352,6 +361,7 @@ def main():
                      "avg_launch_ms": lin_ms_launch, "traffic": traffic},
         "gemm_profile_rank0": r["stats"].get("gemm_profile"),
         "phase_ms_rank0": r["stats"].get("ms"),
+        "timeline_ms_rank0_profiled": r["stats"].get("timeline_ms"),
         "sm_cap_rank0": {k: r["stats"].get(k) for k in ("sm_cap_mode", "sm_applied", "sm_total")},
         "clocks": r["clocks"],
         "cpu_baseline": cpu,

@@ -88,6 +88,10 @@ hexexec_status hexexec_step(hexexec_ctx* ctx, const int32_t* tokens_host, size_t
 hexexec_status hexexec_step_async(hexexec_ctx* ctx, char* err, size_t err_len);
 hexexec_status hexexec_sync(hexexec_ctx* ctx, char* err, size_t err_len);
 hexexec_status hexexec_last_loss(hexexec_ctx* ctx, float* loss_out, char* err, size_t err_len);
+/* Profiling mode (on = 1): steps run eagerly (no graph replay) with a CUDA
+ * event around every GEMM and after every operation; hexexec_stats_json then
+ * reports per-GEMM-class TFLOP/s and a per-kernel-class step timeline. */
+hexexec_status hexexec_set_profile(hexexec_ctx* ctx, int on);
 /* Device timer on the executor's stream: stop = 0 records the start mark;
  * stop = 1 records the end mark, waits for it and returns the elapsed ms. */
 hexexec_status hexexec_timer(hexexec_ctx* ctx, int stop, float* ms_out, char* err,

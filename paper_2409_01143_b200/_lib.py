@@ -57,6 +57,7 @@ hexexec_step_async = _sig("hexexec_step_async", _st, _vp, _c, _sz)
 hexexec_sync = _sig("hexexec_sync", _st, _vp, _c, _sz)
 hexexec_last_loss = _sig("hexexec_last_loss", _st, _vp, C.POINTER(_f), _c, _sz)
 hexexec_timer = _sig("hexexec_timer", _st, _vp, _i, C.POINTER(_f), _c, _sz)
+hexexec_set_profile = _sig("hexexec_set_profile", _st, _vp, _i)
 hexexec_synth_tokens = _sig("hexexec_synth_tokens", _st, _vp, _i64, _vp, _sz, _c, _sz)
 hexexec_tensor_info = _sig("hexexec_tensor_info", _st, _vp, _c, C.POINTER(_i64),
                            C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64))
@@ -88,6 +89,7 @@ EXPORTED = [
     "hexexec_plan_world_size", "hexexec_plan_free", "hexexec_unique_id_size",
     "hexexec_unique_id", "hexexec_ctx_create", "hexexec_ctx_free", "hexexec_step",
     "hexexec_step_async", "hexexec_sync", "hexexec_last_loss", "hexexec_timer",
+    "hexexec_set_profile",
     "hexexec_synth_tokens",
     "hexexec_tensor_info", "hexexec_read_tensor", "hexexec_stats_json", "hexexec_k_gemm",
     "hexexec_k_rmsnorm_fwd", "hexexec_k_rmsnorm_bwd", "hexexec_k_rope", "hexexec_k_softmax_fwd",

@@ -69,6 +69,7 @@ ExecConfig parse_exec_config(const std::string& text) {
       else if (k == "dp_comm_dtype") c.dp_comm_dtype = v.get<std::string>();
       else if (k == "validate_only") c.validate_only = v.get<bool>();
       else if (k == "profile_gemm") c.profile_gemm = v.get<bool>();
+      else if (k == "cuda_graph") c.cuda_graph = v.get<bool>();
       else throw ParseError("exec config: unknown key '" + k + "'");
     } catch (const nlohmann::json::exception& e) {
       throw ParseError("exec config: bad value for '" + k + "'");
@@ -185,7 +186,8 @@ class Executor {
   float* recv_buf = nullptr;  // fwd activations received (fp32 [M,H]) go into slot x[0]
   int64_t step_index = 0;
   // stats
-  cudaEvent_t ev[6] = {};
+  cudaEvent_t ev_eager_[6] = {}, ev_graph_[6] = {};
+  cudaEvent_t* ev = ev_eager_;  // phase events of the mode that ran last
   cudaEvent_t tmr_[2] = {};
   float phase_ms[5] = {0, 0, 0, 0, 0};
   int64_t launches_step = 0, launches_total = 0;
@@ -207,7 +209,9 @@ class Executor {
     tokens_pinned = nullptr;
     if (loss_host) cudaFreeHost(loss_host);
     loss_host = nullptr;
-    for (auto& e : ev)
+    for (auto& e : ev_eager_)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : ev_graph_)
       if (e) cudaEventDestroy(e);
     for (auto& e : tmr_)
       if (e) cudaEventDestroy(e);
@@ -216,6 +220,10 @@ class Executor {
       cudaEventDestroy(r.b);
     }
     gemm_pool_.clear();
+    for (auto& e : mark_pool_) cudaEventDestroy(e);
+    mark_pool_.clear();
+    if (gexec_) cudaGraphExecDestroy(gexec_);
+    gexec_ = nullptr;
     if (own_stream && stream) cudaStreamDestroy(stream);
     stream = nullptr;
   }
@@ -256,7 +264,8 @@ class Executor {
     HX_CUDA(cudaSetDevice(dev));
     HX_CUDA(cudaDeviceGetAttribute(&sm_total, cudaDevAttrMultiProcessorCount, dev));
     setup_stream();
-    for (auto& e : ev) HX_CUDA(cudaEventCreate(&e));
+    for (auto& e : ev_eager_) HX_CUDA(cudaEventCreate(&e));
+    for (auto& e : ev_graph_) HX_CUDA(cudaEventCreate(&e));
     for (auto& e : tmr_) HX_CUDA(cudaEventCreate(&e));
     setup_comms(uid, uid_len);
     if (role.active) {
@@ -438,7 +447,9 @@ class Executor {
       logits = arena.take<float>(M * Vr);
       ce_scr = arena.take<float>(5 * M);
     }
-    loss_acc = arena.take<float>(64);
+    loss_acc = arena.take<float>(32);
+    sp_ = reinterpret_cast<StepParams*>(loss_acc + 16);
+    HX_CUDA(cudaMemsetAsync(sp_, 0, sizeof(StepParams), stream));
     tokens = arena.take<int32_t>(role.batch * (S + 1));
     HX_CUDA(cudaMallocHost(&tokens_pinned, size_t(role.batch * (S + 1)) * 4));
     HX_CUDA(cudaMallocHost(&loss_host, 64));
@@ -496,10 +507,45 @@ class Executor {
   }
 
   // ------------------------------------------------------------ helpers
-  void kcheck() {
+  void kcheck(const char* kind) {
     ++launches_step;
     cudaError_t e = cudaPeekAtLastError();
-    if (e != cudaSuccess) throw CudaError(std::string("kernel launch: ") + cudaGetErrorString(e));
+    if (e != cudaSuccess)
+      throw CudaError(std::string("kernel launch (") + kind + "): " + cudaGetErrorString(e));
+    mark(kind);
+  }
+
+  // step timeline (profile mode): an event after every operation on the stream;
+  // op time = distance to the previous mark (includes any launch gap before it)
+  struct Mark {
+    cudaEvent_t ev;
+    const char* kind;
+  };
+  std::vector<cudaEvent_t> mark_pool_;
+  std::vector<Mark> marks_;
+  std::map<std::string, std::pair<double, int64_t>> timeline_;
+  void mark(const char* kind) {
+    if (!cfg.profile_gemm) return;
+    if (marks_.size() == mark_pool_.size()) {
+      cudaEvent_t e;
+      HX_CUDA(cudaEventCreate(&e));
+      mark_pool_.push_back(e);
+    }
+    cudaEvent_t e = mark_pool_[marks_.size()];
+    HX_CUDA(cudaEventRecord(e, stream));
+    marks_.push_back({e, kind});
+  }
+  void collect_timeline() {
+    timeline_.clear();
+    for (size_t i = 1; i < marks_.size(); ++i) {
+      float ms = 0;
+      if (cudaEventElapsedTime(&ms, marks_[i - 1].ev, marks_[i].ev) == cudaSuccess) {
+        auto& t = timeline_[marks_[i].kind];
+        t.first += ms;
+        t.second += 1;
+      }
+    }
+    marks_.clear();
   }
 
   // GEMM launch; with profile_gemm, each launch is bracketed by CUDA events on
@@ -535,6 +581,7 @@ class Executor {
     if (e != cudaSuccess) throw CudaError(std::string("gemm: ") + cudaGetErrorString(e));
     if (rec) HX_CUDA(cudaEventRecord(rec->b, stream));
     ++launches_step;
+    mark(gemm_kind_ == 0 ? "gemm_linear" : gemm_kind_ == 1 ? "gemm_attention" : "gemm_lm_head");
   }
 
   int64_t steps_since_collect_ = 0;
@@ -575,12 +622,14 @@ class Executor {
     if (role.tp <= 1) return;
     HX_NCCL(ncclAllReduce(buf, buf, size_t(n), ncclBfloat16, ncclSum, tp_comm(), stream));
     ++nccl_calls_step;
+    mark("nccl_tp_allreduce");
   }
 
   void tp_allreduce_f32(const float* in, float* out, int64_t n, ncclRedOp_t op) {
     if (role.tp <= 1) return;
     HX_NCCL(ncclAllReduce(in, out, size_t(n), ncclFloat32, op, tp_comm(), stream));
     ++nccl_calls_step;
+    mark("nccl_tp_allreduce");
   }
 
   int32_t* tok_of(int64_t mbi) { return tokens + mbi * mb * (S + 1); }
@@ -594,27 +643,27 @@ class Executor {
     const float eps = float(L.model.norm_eps);
     // attention block
     k_rmsnorm_fwd(x_in, nullptr, nullptr, w.attn_norm.p32, a.xn, a.rstd1, int(M), int(H), eps, stream);
-    kcheck();
+    kcheck("rmsnorm_fwd");
     gemm(g2(M, qkvw, H, a.xn, 0, H, w.wqkv.p16, 0, H, a.qkv, qkvw, 0));
     k_rope(a.qkv, int(M), int(S), int(nh), int(d), float(L.model.rope_theta), 0, stream);
-    kcheck();
+    kcheck("rope");
     attention_fwd(a);
     if (role.tp == 1) {
       GemmDesc g = g2(M, H, kr, a.attn, 0, kr, w.wo.p16, 1, H, a.x_mid, H, 1);
       g.R = x_in;
       gemm(g);
       k_rmsnorm_fwd(a.x_mid, nullptr, nullptr, w.mlp_norm.p32, a.hn, a.rstd2, int(M), int(H), eps, stream);
-      kcheck();
+      kcheck("rmsnorm_fwd");
     } else {
       gemm(g2(M, H, kr, a.attn, 0, kr, w.wo.p16, 1, H, ypart, H, 0));
       tp_allreduce_bf16(ypart, M * H);
       k_rmsnorm_fwd(x_in, ypart, a.x_mid, w.mlp_norm.p32, a.hn, a.rstd2, int(M), int(H), eps, stream);
-      kcheck();
+      kcheck("rmsnorm_fwd");
     }
     // MLP block
     gemm(g2(M, 2 * F, H, a.hn, 0, H, w.wgu.p16, 0, H, a.gu, 2 * F, 0));
     k_swiglu_fwd(a.gu, a.act, int(M), int(F), stream);
-    kcheck();
+    kcheck("swiglu_fwd");
     if (role.tp == 1) {
       GemmDesc g = g2(M, H, F, a.act, 0, F, w.wdown.p16, 1, H, x_out, H, 1);
       g.R = a.x_mid;
@@ -623,7 +672,7 @@ class Executor {
       gemm(g2(M, H, F, a.act, 0, F, w.wdown.p16, 1, H, ypart, H, 0));
       tp_allreduce_bf16(ypart, M * H);
       k_residual_add(a.x_mid, ypart, x_out, M * H, stream);
-      kcheck();
+      kcheck("residual_add");
     }
   }
 
@@ -649,7 +698,7 @@ class Executor {
     g.causal = kCausalSkipUpper;
     gemm(g);
     k_softmax_fwd(scores, a.P, int(S), int(mb * nh), stream);
-    kcheck();
+    kcheck("softmax_fwd");
     GemmDesc o;
     o.M = int(S);
     o.N = int(d);
@@ -670,7 +719,7 @@ class Executor {
   void head_fwd(Slot& sl, int64_t mbi) {
     const float eps = float(L.model.norm_eps);
     k_rmsnorm_fwd(sl.x[size_t(nl)], nullptr, nullptr, final_norm.p32, sl.xf, sl.rstdf, int(M), int(H), eps, stream);
-    kcheck();
+    kcheck("rmsnorm_fwd");
     gemm_kind_ = 2;
     gemm(g2(M, Vr, H, sl.xf, 0, H, lm_head.p16, 0, H, logits, Vr, 1));
     gemm_kind_ = 0;
@@ -680,11 +729,11 @@ class Executor {
     float* gmax = ce_scr + 4 * M;
     const int32_t* tk = tok_of(mbi);
     k_ce_stats(logits, int(Vr), int(v0), tk, int(M), int(S), lmax, lsum, st2, stream);
-    kcheck();
+    kcheck("ce_stats");
     if (role.tp > 1) {
       tp_allreduce_f32(lmax, gmax, M, ncclMax);
       k_ce_rescale(lmax, lsum, gmax, st2, int(M), stream);
-      kcheck();
+      kcheck("ce_rescale");
       tp_allreduce_f32(st2, st2, 2 * M, ncclSum);
     } else {
       HX_CUDA(cudaMemcpyAsync(gmax, lmax, size_t(M) * 4, cudaMemcpyDeviceToDevice, stream));
@@ -692,13 +741,13 @@ class Executor {
     const float inv_count = 1.f / float(role.batch * S);
     k_ce_finish(logits, int(Vr), int(v0), tk, int(M), int(S), gmax, st2, inv_count, sl.dlogits,
                 loss_acc, stream);
-    kcheck();
+    kcheck("ce_finish");
   }
 
   void forward(int64_t mbi, Slot& sl) {
     if (role.first_stage) {
       k_embed_fwd(tok_of(mbi), embed.p32, sl.x[0], int(M), int(S), int(H), stream);
-      kcheck();
+      kcheck("embed_fwd");
     }
     for (int64_t l = 0; l < nl; ++l) layer_fwd(sl, l);
     if (role.last_stage) head_fwd(sl, mbi);
@@ -718,7 +767,7 @@ class Executor {
       gemm(g);
     }
     k_swiglu_bwd(a.gu, da, dgu, int(M), int(F), stream);
-    kcheck();
+    kcheck("swiglu_bwd");
     gemm(g2(M, H, 2 * F, dgu, 0, 2 * F, w.wgu.p16, 1, H, dy16, H, 0));
     {
       GemmDesc g = g2(2 * F, H, M, dgu, 1, 2 * F, a.hn, 1, H, w.wgu.g32, H, 1);
@@ -731,7 +780,7 @@ class Executor {
     bf16* dxmb = dxib;
     k_rmsnorm_bwd(dy16, nullptr, a.x_mid, a.rstd2, w.mlp_norm.p32, dxo, dxm, dxmb, w.mlp_norm.g32,
                   int(M), int(H), coef_, stream);
-    kcheck();
+    kcheck("rmsnorm_bwd");
     // attention: O projection
     gemm(g2(M, kr, H, dxmb, 0, H, w.wo.p16, 0, H, dattn, kr, 0));
     {
@@ -741,7 +790,7 @@ class Executor {
     }
     attention_bwd(a);
     k_rope(dqkv, int(M), int(S), int(nh), int(d), float(L.model.rope_theta), 1, stream);
-    kcheck();
+    kcheck("rope");
     gemm(g2(M, H, qkvw, dqkv, 0, qkvw, w.wqkv.p16, 1, H, dy16, H, 0));
     {
       GemmDesc g = g2(qkvw, H, M, dqkv, 1, qkvw, a.xn, 1, H, w.wqkv.g32, H, 1);
@@ -752,7 +801,7 @@ class Executor {
     // dx_in = dx_mid + rmsnorm_bwd(dxn): in place over dx_mid (row-local)
     k_rmsnorm_bwd(dy16, nullptr, sl.x[size_t(l)], a.rstd1, w.attn_norm.p32, dxm, dxi, dxib,
                   w.attn_norm.g32, int(M), int(H), coef_, stream);
-    kcheck();
+    kcheck("rmsnorm_bwd");
   }
 
   void attention_bwd(LayerActs& a) {
@@ -775,7 +824,7 @@ class Executor {
     g.causal = kCausalSkipUpper;
     gemm(g);
     k_softmax_bwd(a.P, dP, dS, 1.f / std::sqrt(float(d)), int(S), int(mb * nh), stream);
-    kcheck();
+    kcheck("softmax_bwd");
     // dQ = dS K
     GemmDesc q;
     q.M = int(S);
@@ -824,11 +873,11 @@ class Executor {
       tp_allreduce_bf16(dy16, M * H);
       k_rmsnorm_bwd(dy16, nullptr, sl.x[size_t(nl)], sl.rstdf, final_norm.p32, nullptr, cur, curb,
                     final_norm.g32, int(M), int(H), coef_, stream);
-      kcheck();
+      kcheck("rmsnorm_bwd");
     } else {
       HX_CUDA(cudaMemcpyAsync(cur, dx_top, size_t(M * H) * 4, cudaMemcpyDeviceToDevice, stream));
       k_cast_bf16(cur, curb, M * H, stream);
-      kcheck();
+      kcheck("cast_bf16");
     }
     for (int64_t l = nl - 1; l >= 0; --l) {
       // dxi aliases the ping-pong partner; dxb reused in place (row-local ops)
@@ -837,7 +886,7 @@ class Executor {
     }
     if (role.first_stage) {
       k_embed_bwd(tok_of(mbi), cur, embed.g32, int(M), int(S), int(H), stream);
-      kcheck();
+      kcheck("embed_bwd");
     }
     bwd_out_ = cur;
   }
@@ -890,13 +939,17 @@ class Executor {
       ++next_bwd;
     };
     // warm-up forwards
+    const bool pp = P > 1;
     for (int64_t i = 0; i < warm; ++i) {
       Slot& sl = slot_of(i);
       recv_fwd(sl);
+      if (pp) mark("nccl_pp");
       forward(i, sl);
       send_fwd(sl);
+      if (pp) mark("nccl_pp");
     }
     if (rem > 0) recv_fwd(slot_of(warm));
+    if (pp) mark("nccl_pp");
     for (int64_t i = 0; i < rem; ++i) {
       const int64_t f = warm + i;
       Slot& sl = slot_of(f);
@@ -906,16 +959,20 @@ class Executor {
       send_fwd(sl);
       recv_bwd(grecv);
       HX_NCCL(ncclGroupEnd());
+      if (pp) mark("nccl_pp");
       do_bwd(i);
       HX_NCCL(ncclGroupStart());
       send_bwd(bwd_out_);
       if (i + 1 < rem) recv_fwd(slot_of(f + 1));
       HX_NCCL(ncclGroupEnd());
+      if (pp) mark("nccl_pp");
     }
     for (int64_t i = rem; i < n; ++i) {
       recv_bwd(grecv);
+      if (pp) mark("nccl_pp");
       do_bwd(i);
       send_bwd(bwd_out_);
+      if (pp) mark("nccl_pp");
     }
   }
 
@@ -933,7 +990,7 @@ class Executor {
         k_scale_cast(G32 + rt.offset, G16 + rt.offset, cnt, sc, stream);
       else
         k_scale(G32 + rt.offset, cnt, sc, stream);
-      kcheck();
+      kcheck("scale");
     }
     // 2. chunk-matched allreduce, one NCCL call per bucket (grouped)
     if (!buckets.empty()) {
@@ -948,6 +1005,7 @@ class Executor {
         ++nccl_calls_step;
       }
       HX_NCCL(ncclGroupEnd());
+      mark("nccl_dp_allreduce");
     }
     cudaEventRecord(ev[3], stream);
     // 3. AdamW per tensor (weight decay only on matrices)
@@ -963,8 +1021,8 @@ class Executor {
       const float* g32 = g16 ? nullptr : G32 + rt.offset;
       const float gscale = cov ? 1.f : float(role.dp_weight / double(rt.multiplicity));
       k_adamw(P32 + rt.offset, P16 + rt.offset, Mo + rt.offset, Vo + rt.offset, g16, g32, cnt,
-              gscale, cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, wd, bc1, bc2, stream);
-      kcheck();
+              gscale, cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, wd, bc1, bc2, stream, sp_);
+      kcheck("adamw");
     }
     cudaEventRecord(ev[4], stream);
   }
@@ -981,6 +1039,14 @@ class Executor {
     return c == cnt;
   }
 
+  // ------------------------------------------------------------ graph replay
+  // After one eager step (NCCL / lazy init warm-up), the whole step -- every
+  // kernel, memset, NCCL call and timing event -- is captured once into a CUDA
+  // graph and replayed; per-step scalars live in device StepParams.
+  cudaGraphExec_t gexec_ = nullptr;
+  int64_t graph_launches_ = 0;
+  StepParams* sp_ = nullptr;
+
   void step_enqueue() {
     if (!role.active) {
       // idle device: still joins the world loss reduction (contributes 0)
@@ -989,13 +1055,49 @@ class Executor {
       ++step_index;
       return;
     }
+    const bool gen = tokens_from_host_ == nullptr && (role.first_stage || role.last_stage);
+    HX_CUDA(cudaMemsetAsync(&sp_->gen_tokens, gen ? 1 : 0, sizeof(int), stream));
+    const bool graph = cfg.cuda_graph && !cfg.profile_gemm;
+    (void)cudaGetLastError();  // clear non-sticky errors (e.g. a not-ready event query)
+    if (graph && gexec_) {
+      ev = ev_graph_;
+      HX_CUDA(cudaGraphLaunch(gexec_, stream));
+      launches_step = graph_launches_;
+    } else if (graph && step_index >= 1) {
+      ev = ev_graph_;  // the graph owns its own phase events
+      HX_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeRelaxed));
+      cudaGraph_t g = nullptr;
+      try {
+        enqueue_body();
+      } catch (...) {
+        cudaStreamEndCapture(stream, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      HX_CUDA(cudaStreamEndCapture(stream, &g));
+      cudaError_t e = cudaGraphInstantiate(&gexec_, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) throw CudaError(std::string("graph instantiate: ") + cudaGetErrorString(e));
+      graph_launches_ = launches_step;
+      HX_CUDA(cudaGraphLaunch(gexec_, stream));
+    } else {
+      ev = ev_eager_;
+      enqueue_body();
+    }
+    launches_total += launches_step;
+    ++step_index;
+  }
+
+  void enqueue_body() {
     launches_step = 0;
     nccl_calls_step = 0;
     cudaEventRecord(ev[0], stream);
-    if (tokens_from_host_ == nullptr && (role.first_stage || role.last_stage)) {
-      k_gen_tokens(tokens, role.batch, int(S), role.sample0, cfg.seed, step_index,
-                   int(L.model.vocab_size), stream);
-      kcheck();
+    k_step_tick(sp_, cfg.beta1, cfg.beta2, stream);
+    kcheck("step_tick");
+    if (role.first_stage || role.last_stage) {
+      k_gen_tokens(tokens, role.batch, int(S), role.sample0, cfg.seed, 0,
+                   int(L.model.vocab_size), stream, sp_);
+      kcheck("gen_tokens");
     }
     HX_CUDA(cudaMemsetAsync(loss_acc, 0, 4, stream));
     // zero the atomically-accumulated grads (norm gains, embedding)
@@ -1004,13 +1106,12 @@ class Executor {
       if (ts.id == kAttnNorm || ts.id == kMlpNorm || ts.id == kFinalNorm || ts.id == kEmbed)
         HX_CUDA(cudaMemsetAsync(G32 + rt.offset, 0, size_t(rt.rows * ts.cols) * 4, stream));
     }
+    mark("prologue");
     cudaEventRecord(ev[1], stream);
     run_pipeline();
     dp_sync_and_update();
     finish_loss();
     cudaEventRecord(ev[5], stream);
-    launches_total += launches_step;
-    ++step_index;
   }
 
   void finish_loss() {
@@ -1041,6 +1142,7 @@ class Executor {
     if (role.active) collect_times();
     steps_since_collect_ = 1;
     collect_gemm_profile();
+    collect_timeline();
     if (loss_out) *loss_out = last_loss;
   }
 
@@ -1051,6 +1153,7 @@ class Executor {
     if (cudaEventElapsedTime(&t, ev[2], ev[3]) == cudaSuccess) phase_ms[2] = t;
     if (cudaEventElapsedTime(&t, ev[3], ev[4]) == cudaSuccess) phase_ms[3] = t;
     if (cudaEventElapsedTime(&t, ev[0], ev[5]) == cudaSuccess) phase_ms[4] = t;
+    (void)cudaGetLastError();
   }
 
   std::string stats() const {
@@ -1080,6 +1183,9 @@ class Executor {
                        {"tflops", gemm_ms_[k] > 0 ? gemm_flops_[k] / gemm_ms_[k] / 1e9 : 0.0}};
       g["steps"] = steps_since_collect_;
       j["gemm_profile"] = g;
+      ojson tl;
+      for (const auto& [k, v] : timeline_) tl[k] = {{"ms", v.first}, {"ops", v.second}};
+      j["timeline_ms"] = tl;
     }
     return j.dump();
   }
@@ -1108,6 +1214,8 @@ void executor_step_async(Executor& e) {
   ++e.steps_since_collect_;
 }
 
+void executor_set_profile(Executor& e, bool on) { e.cfg.profile_gemm = on; }
+
 void executor_timer(Executor& e, int stop, float* ms) {
   if (!stop) {
     HX_CUDA(cudaEventRecord(e.tmr_[0], e.stream));
@@ -1124,6 +1232,7 @@ void executor_sync(Executor& e) {
   e.last_loss = e.loss_host[0] / float(e.L.plan.global_batch * e.S);
   if (e.role.active) e.collect_times();
   e.collect_gemm_profile();
+  e.collect_timeline();
 }
 
 float executor_last_loss(Executor& e) { return e.last_loss; }

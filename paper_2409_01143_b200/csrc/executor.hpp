@@ -17,7 +17,8 @@ struct ExecConfig {
   std::string sm_cap = "green";       // "green" | "cta" | "none"
   std::string dp_comm_dtype = "bf16"; // "bf16" | "fp32"
   bool validate_only = false;
-  bool profile_gemm = false;          // per-GEMM CUDA events (roofline evidence)
+  bool profile_gemm = false;          // per-GEMM CUDA events (roofline evidence); eager
+  bool cuda_graph = true;             // replay the captured step graph (after step 0)
 };
 
 ExecConfig parse_exec_config(const std::string& text);
@@ -33,6 +34,7 @@ void executor_step_async(Executor& e);
 void executor_sync(Executor& e);
 // device time between a start (stop=0) and stop (stop=1) mark on the executor stream
 void executor_timer(Executor& e, int stop, float* ms);
+void executor_set_profile(Executor& e, bool on);
 float executor_last_loss(Executor& e);
 void executor_synth_tokens(const Executor& e, int64_t step, int32_t* out, size_t n);
 bool executor_tensor_info(const Executor& e, const std::string& name, int64_t* row0,

@@ -50,5 +50,7 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream);
 
 // number of SMs the GEMM may occupy (0 = all); used for SM-capped ranks
 void gemm_set_sm_limit(int sms);
+// 0 = auto (CTA pairs when M > 128), 1 / 2 = force single-SM / paired tiles
+void gemm_force_cta_group(int cg);
 
 }  // namespace hexexec

@@ -1,19 +1,24 @@
 // Persistent warp-specialised tcgen05 GEMM for sm_100a.
 //
-// Roles (256 threads):  warp 0 = TMA producer (one elected lane),
-//                       warp 1 = MMA issuer (one elected lane),
-//                       warp 2 = TMEM allocator,
-//                       warps 4..7 = epilogue (TMEM -> registers -> global).
-// Operands stream through a STAGES-deep shared-memory ring (mbarrier
-// full/empty pairs); the fp32 accumulator is double-buffered in TMEM
-// (2 x BN columns) so the epilogue of tile t overlaps the mainloop of t+1.
-// Tile shape 128 x BN x 64, UMMA 128 x BN x 16, SWIZZLE_128B operand tiles.
-// K-major operands are loaded as one TMA box [rows][64]; MN-major operands as
-// (rows/64) boxes [64 k][64 mn], giving the canonical MN-major UMMA layout
-// (LBO = 64*128 B between MN atoms, SBO = 1024 B between 8-row k groups).
+// Roles (256 threads per CTA):  warp 0 = TMA producer (one elected lane),
+//                               warp 1 = MMA issuer (one lane, leader CTA only),
+//                               warp 2 = TMEM allocator,
+//                               warps 4..7 = epilogue (TMEM -> registers -> global).
+// CG = 2 runs CTA pairs (cluster of 2, `cta_group::2`): one 256 x BN x 16 UMMA
+// per k-step spans both SMs; each CTA stages its 128 rows of A and BN/2 rows of
+// B, TMA completion is counted on the leader's mbarrier, the leader issues the
+// MMAs and multicasts tcgen05.commit to both CTAs; each CTA's TMEM holds its
+// 128 accumulator rows.  CG = 1 is the single-SM variant (M < 256 problems).
+// Operands stream through a STAGES-deep smem ring (full/empty mbarriers); the
+// fp32 accumulator is double-buffered in TMEM (2 x BN columns) so the
+// epilogue of tile t overlaps the mainloop of tile t+1.  SWIZZLE_128B tiles:
+// K-major operands as one TMA box [rows][64]; MN-major operands as (rows/64)
+// boxes [64 k][64 mn] (canonical MN-major UMMA layout: LBO = 64*128 B between
+// MN atoms, SBO = 1024 B between 8-row k groups).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <mutex>
 
@@ -24,7 +29,7 @@ namespace hexexec {
 
 namespace {
 
-constexpr int BM = 128;
+constexpr int BM = 128;  // rows per CTA
 constexpr int BK = 64;
 constexpr int kThreads = 256;
 
@@ -39,23 +44,44 @@ struct EpiParams {
   int m_tiles, n_tiles, num_tiles;
 };
 
-template <int BN>
+template <int BN, int CG>
 struct Cfg {
-  static constexpr int STAGES = BN >= 256 ? 4 : 6;
+  static constexpr int TM = BM * CG;         // rows per (pair) tile
+  static constexpr int BNC = BN / CG;        // B rows staged per CTA
   static constexpr uint32_t A_BYTES = BM * BK * 2;
-  static constexpr uint32_t B_BYTES = BN * BK * 2;
+  static constexpr uint32_t B_BYTES = BNC * BK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-  static constexpr size_t SMEM = 1024 /*align slack*/ + size_t(STAGES) * STAGE_BYTES + 256;
+  // epilogue staging per epilogue warp: 2 x [32 rows][32 cols] fp32 store buffers
+  // (TMA store / reduce-add sources) + 1 buffer for the residual tile (TMA load)
+  static constexpr uint32_t EPI_CHUNK = 32 * 32 * 4;
+  static constexpr uint32_t EPI_WARP = 3 * EPI_CHUNK;
+  static constexpr uint32_t EPI_BYTES = 4 * EPI_WARP;
+  // 227 KB opt-in dynamic smem per CTA, minus alignment slack, epilogue, barriers
+  static constexpr uint32_t MAIN_BUDGET = 232448u - 1024u - 256u - EPI_BYTES;
+  static constexpr int STAGES = int(MAIN_BUDGET / STAGE_BYTES) > 8 ? 8 : int(MAIN_BUDGET / STAGE_BYTES);
+  static constexpr uint32_t TMEM_COLS = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
+  static constexpr size_t SMEM =
+      1024 /*align slack*/ + size_t(STAGES) * STAGE_BYTES + EPI_BYTES + 256;
 };
 
-HX_DEVICE bool tile_skipped(const EpiParams& p, int m0, int n0) {
-  return p.causal == kCausalSkipUpper && n0 > m0 + BM - 1;
+// byte offset of the 16-byte chunk `chunk` of row `row` inside a [32][row_bytes]
+// tile staged for a SWIZZLE_128B (row_bytes 128) / SWIZZLE_64B (row_bytes 64) TMA box
+template <int ROW_BYTES>
+HX_DEVICE uint32_t swz(int row, int chunk) {
+  const uint32_t off = uint32_t(row * ROW_BYTES + chunk * 16);
+  constexpr uint32_t mask = ROW_BYTES == 128 ? 7u : 3u;
+  return off ^ (((off >> 7) & mask) << 4);
 }
 
+template <int TM>
+HX_DEVICE bool tile_skipped(const EpiParams& p, int m0, int n0) {
+  return p.causal == kCausalSkipUpper && n0 > m0 + TM - 1;
+}
+
+template <int TM>
 HX_DEVICE void k_range(const EpiParams& p, int m0, int& kb0, int& kb1) {
   int k_begin = 0, k_end = p.K;
-  if (p.causal == kCausalKLower) k_end = min(p.K, m0 + BM);
+  if (p.causal == kCausalKLower) k_end = min(p.K, m0 + TM);
   if (p.causal == kCausalKUpper) k_begin = (m0 / BK) * BK;
   kb0 = k_begin / BK;
   kb1 = (k_end + BK - 1) / BK;
@@ -64,33 +90,43 @@ HX_DEVICE void k_range(const EpiParams& p, int m0, int& kb0, int& kb1) {
 
 // tile t -> (m0, n-tile index, batch coords); n fastest so CTAs of one wave
 // share the A row-panel in L2
+template <int TM>
 HX_DEVICE void decode_tile(const EpiParams& p, int t, int& m0, int& nt, int& z1, int& z2) {
   nt = t % p.n_tiles;
   int r = t / p.n_tiles;
-  m0 = (r % p.m_tiles) * BM;
+  m0 = (r % p.m_tiles) * TM;
   int z = r / p.m_tiles;
   z1 = z % p.nb1;
   z2 = z / p.nb1;
 }
 
-template <int BN, int A_MN, int B_MN>
+template <int BN, int A_MN, int B_MN, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmR,
                 const EpiParams p) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, CG>;
   constexpr int ST = C::STAGES;
+  constexpr int TM = C::TM;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + ST * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * C::STAGE_BYTES);
+  uint8_t* sEpi = smem + ST * C::STAGE_BYTES;  // 1024-aligned (stage sizes are multiples of 1 KB)
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + C::EPI_BYTES);
   uint64_t* empty = full + ST;
   uint64_t* tfull = empty + ST;   // [2]
   uint64_t* tempty = tfull + 2;   // [2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rbar = tempty + 2;    // [4] residual-tile loads, one per epilogue warp
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(rbar + 4);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;
+  const bool leader = crank == 0;
+  // pair index and pair count (persistent loop over pair tiles)
+  const int pid = blockIdx.x / CG;
+  const int npairs = gridDim.x / CG;
 
   if (threadIdx.x == 0) {
     tma_prefetch(&tmA);
@@ -101,47 +137,79 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], 4 * CG);
     }
+    for (int i = 0; i < 4; ++i) mbar_init(&rbar[i], 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<C::TMEM_COLS>(tslot);
+  if (warp == 3 && lane == 0) {
+    tma_prefetch(&tmC);
+    if (p.R) tma_prefetch(&tmR);
+  }
+  if (warp == 2) {
+    if (CG == 2)
+      tmem_alloc_2sm<C::TMEM_COLS>(tslot);
+    else
+      tmem_alloc<C::TMEM_COLS>(tslot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer
+      // ---------------- TMA producer (both CTAs of a pair)
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      for (int t = pid; t < p.num_tiles; t += npairs) {
         int m0, nt, z1, z2;
-        decode_tile(p, t, m0, nt, z1, z2);
+        decode_tile<TM>(p, t, m0, nt, z1, z2);
         int n0 = nt * BN;
-        if (tile_skipped(p, m0, n0)) continue;
+        if (tile_skipped<TM>(p, m0, n0)) continue;
         int kb0, kb1;
-        k_range(p, m0, kb0, kb1);
+        k_range<TM>(p, m0, kb0, kb1);
+        const int am = m0 + BM * int(crank);      // this CTA's A rows
+        const int bn = n0 + C::BNC * int(crank);  // this CTA's B rows
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          if (leader) mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES * CG);
           uint8_t* a = sA + stage * C::A_BYTES;
           uint8_t* b = sB + stage * C::B_BYTES;
           int k0 = kb * BK;
-          if (A_MN) {
+          if (CG == 2) {
+            if (A_MN) {
 #pragma unroll
-            for (int c = 0; c < BM / 64; ++c)
-              tma_load_4d(a + c * (BK * 128), &tmA, &full[stage], m0 + c * 64, k0, z1, z2);
-          } else {
-            tma_load_4d(a, &tmA, &full[stage], k0, m0, z1, z2);
-          }
-          if (B_MN) {
+              for (int c = 0; c < BM / 64; ++c)
+                tma_load_4d_2sm(a + c * (BK * 128), &tmA, &full[stage], am + c * 64, k0, z1, z2);
+            } else {
+              tma_load_4d_2sm(a, &tmA, &full[stage], k0, am, z1, z2);
+            }
+            if (B_MN) {
 #pragma unroll
-            for (int c = 0; c < BN / 64; ++c)
-              tma_load_4d(b + c * (BK * 128), &tmB, &full[stage], n0 + c * 64, k0, z1, z2);
+              for (int c = 0; c < C::BNC / 64; ++c)
+                tma_load_4d_2sm(b + c * (BK * 128), &tmB, &full[stage], bn + c * 64, k0, z1, z2);
+            } else {
+              tma_load_4d_2sm(b, &tmB, &full[stage], k0, bn, z1, z2);
+            }
           } else {
-            tma_load_4d(b, &tmB, &full[stage], k0, n0, z1, z2);
+            if (A_MN) {
+#pragma unroll
+              for (int c = 0; c < BM / 64; ++c)
+                tma_load_4d(a + c * (BK * 128), &tmA, &full[stage], am + c * 64, k0, z1, z2);
+            } else {
+              tma_load_4d(a, &tmA, &full[stage], k0, am, z1, z2);
+            }
+            if (B_MN) {
+#pragma unroll
+              for (int c = 0; c < C::BNC / 64; ++c)
+                tma_load_4d(b + c * (BK * 128), &tmB, &full[stage], bn + c * 64, k0, z1, z2);
+            } else {
+              tma_load_4d(b, &tmB, &full[stage], k0, bn, z1, z2);
+            }
           }
           if (++stage == ST) {
             stage = 0;
@@ -151,22 +219,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer
+    if (lane == 0 && leader) {
+      // ---------------- MMA issuer (leader CTA)
       constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(A_MN) << 15) |
                                  (uint32_t(B_MN) << 16) | (uint32_t(BN >> 3) << 17) |
-                                 (uint32_t(BM >> 4) << 24);
+                                 (uint32_t(TM >> 4) << 24);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      for (int t = pid; t < p.num_tiles; t += npairs) {
         int m0, nt, z1, z2;
-        decode_tile(p, t, m0, nt, z1, z2);
+        decode_tile<TM>(p, t, m0, nt, z1, z2);
         int n0 = nt * BN;
-        if (tile_skipped(p, m0, n0)) continue;
+        if (tile_skipped<TM>(p, m0, n0)) continue;
         int kb0, kb1;
-        k_range(p, m0, kb0, kb1);
+        k_range<TM>(p, m0, kb0, kb1);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t dtm = tbase + uint32_t(acc * BN);
@@ -181,15 +249,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                                : umma_desc_sw128(a_addr + ks * 32, 16, 1024);
             uint64_t bd = B_MN ? umma_desc_sw128(b_addr + ks * 2048, BK * 128, 1024)
                                : umma_desc_sw128(b_addr + ks * 32, 16, 1024);
-            tc_mma_f16(dtm, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
+            if (CG == 2)
+              tc_mma_f16_2sm(dtm, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
+            else
+              tc_mma_f16(dtm, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
           }
-          tc_commit(&empty[stage]);
+          if (CG == 2)
+            tc_commit_2sm_mc(&empty[stage], 0x3);
+          else
+            tc_commit(&empty[stage]);
           if (++stage == ST) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(&tfull[acc]);
+        if (CG == 2)
+          tc_commit_2sm_mc(&tfull[acc], 0x3);
+        else
+          tc_commit(&tfull[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -197,98 +274,112 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue
+    // ---------------- epilogue (both CTAs; each owns 128 accumulator rows)
+    // TMEM -> registers (x alpha, + residual tile loaded by TMA) -> swizzled
+    // smem chunk [32 rows][32 cols] -> TMA store (or TMA reduce-add for beta)
     const int ew = warp - 4;  // TMEM lanes 32*ew .. 32*ew+31
+    uint8_t* ebuf = sEpi + ew * C::EPI_WARP;  // two store buffers
+    uint8_t* rbuf = ebuf + 2 * C::EPI_CHUNK;  // residual tile
     int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    uint32_t acc_phase = 0, rphase = 0;
+    int sb = 0;
+    for (int t = pid; t < p.num_tiles; t += npairs) {
       int m0, nt, z1, z2;
-      decode_tile(p, t, m0, nt, z1, z2);
+      decode_tile<TM>(p, t, m0, nt, z1, z2);
       int n0 = nt * BN;
-      if (tile_skipped(p, m0, n0)) continue;
+      if (tile_skipped<TM>(p, m0, n0)) continue;
       int kb0, kb1;
-      k_range(p, m0, kb0, kb1);
+      k_range<TM>(p, m0, kb0, kb1);
       const bool have = kb1 > kb0;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = m0 + ew * 32 + lane;
-      const long long cbase = z1 * p.cbs1 + z2 * p.cbs2 + (long long)row * p.ldc;
+      const int row0 = m0 + BM * int(crank) + ew * 32;  // this warp's 32-row slab
+      if (row0 < p.M) {
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tbase + (uint32_t(ew * 32) << 16) + uint32_t(acc * BN + c), r);
-        tmem_ld_wait();
-        const int col = n0 + c;
-        if (row >= p.M || col >= p.N) continue;
-        float v[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = have ? __uint_as_float(r[i]) * p.alpha : 0.f;
-        const bool full_chunk = col + 32 <= p.N;
-        if (p.c_fp32) {
-          float* out = reinterpret_cast<float*>(p.C) + cbase + col;
-          const float* res = p.R ? p.R + cbase + col : nullptr;
-          if (full_chunk && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
-            float4* o4 = reinterpret_cast<float4*>(out);
-            // issue every load of the chunk before the first store (no aliasing
-            // stalls: 8 independent 16-byte loads in flight per thread)
-            if (p.beta || res) {
-              float4 o[8];
-              const float4* src = p.beta ? o4 : reinterpret_cast<const float4*>(res);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) o[i] = __ldcs(src + i);
-              if (p.beta && res) {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                  float4 q = __ldcs(reinterpret_cast<const float4*>(res) + i);
-                  o[i].x += q.x; o[i].y += q.y; o[i].z += q.z; o[i].w += q.w;
-                }
-              }
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                v[4 * i] += o[i].x; v[4 * i + 1] += o[i].y;
-                v[4 * i + 2] += o[i].z; v[4 * i + 3] += o[i].w;
-              }
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              o4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-          } else {
-            for (int i = 0; i < 32 && col + i < p.N; ++i)
-              out[i] = (p.beta ? out[i] : 0.f) + (res ? res[i] : 0.f) + v[i];
+        for (int c = 0; c < BN; c += 32) {
+          const int col = n0 + c;
+          if (col >= p.N) break;
+          if (p.R && lane == 0) {
+            mbar_arrive_expect_tx(&rbar[ew], C::EPI_CHUNK);
+            tma_load_4d(rbuf, &tmR, &rbar[ew], col, row0, z1, z2);
           }
-        } else {
-          __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.C) + cbase + col;
-          if (full_chunk && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
-            uint4* o4 = reinterpret_cast<uint4*>(out);
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tbase + (uint32_t(ew * 32) << 16) + uint32_t(acc * BN + c), r);
+          tmem_ld_wait();
+          float v[32];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
+          for (int i = 0; i < 32; ++i) v[i] = have ? __uint_as_float(r[i]) * p.alpha : 0.f;
+          if (p.R) {
+            mbar_wait(&rbar[ew], rphase);
+            rphase ^= 1;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              float4 o = *reinterpret_cast<const float4*>(rbuf + swz<128>(lane, q));
+              v[4 * q] += o.x;
+              v[4 * q + 1] += o.y;
+              v[4 * q + 2] += o.z;
+              v[4 * q + 3] += o.w;
+            }
+          }
+          // the buffer written now was the source of the store two chunks ago
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+          uint8_t* sbuf = ebuf + sb * C::EPI_CHUNK;
+          if (p.c_fp32) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              *reinterpret_cast<float4*>(sbuf + swz<128>(lane, q)) =
+                  make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
               uint4 w;
-              w.x = pack_bf16x2(v[8 * i + 0], v[8 * i + 1]);
-              w.y = pack_bf16x2(v[8 * i + 2], v[8 * i + 3]);
-              w.z = pack_bf16x2(v[8 * i + 4], v[8 * i + 5]);
-              w.w = pack_bf16x2(v[8 * i + 6], v[8 * i + 7]);
-              o4[i] = w;
+              w.x = pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+              w.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+              w.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+              w.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+              *reinterpret_cast<uint4*>(sbuf + swz<64>(lane, q)) = w;
             }
-          } else {
-            for (int i = 0; i < 32 && col + i < p.N; ++i) out[i] = __float2bfloat16_rn(v[i]);
           }
+          fence_async_shared();
+          __syncwarp();
+          if (lane == 0) {
+            if (p.beta)
+              tma_reduce_add_4d(&tmC, sbuf, col, row0, z1, z2);
+            else
+              tma_store_4d(&tmC, sbuf, col, row0, z1, z2);
+            bulk_commit();
+          }
+          sb ^= 1;
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (CG == 2)
+          mbar_arrive_cluster(&tempty[acc], 0);  // the leader's MMA waits on both CTAs
+        else
+          mbar_arrive(&tempty[acc]);
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) bulk_wait_all();
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<C::TMEM_COLS>(tbase);
+    if (CG == 2)
+      tmem_dealloc_2sm<C::TMEM_COLS>(tbase);
+    else
+      tmem_dealloc<C::TMEM_COLS>(tbase);
   }
 }
 
@@ -297,6 +388,7 @@ PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
 int g_sm_limit = 0;
 int g_num_sms = 0;
+int g_force_cg = 0;  // 0 = auto, 1 / 2 = force (tests)
 
 cudaError_t load_encode() {
   std::call_once(g_encode_once, [] {
@@ -313,7 +405,7 @@ cudaError_t load_encode() {
   return g_encode ? cudaSuccess : cudaErrorNotSupported;
 }
 
-// 4D map over a bf16 operand: dim0 contiguous.  rows_box = box extent on dim1.
+// 4D map over a bf16 operand: dim0 contiguous; box {box0, box1, 1, 1}
 bool make_map(CUtensorMap* map, const GemmOperand& op, long long d0, long long d1, int nb1,
               int nb2, uint32_t box0, uint32_t box1) {
   cuuint64_t dims[4] = {cuuint64_t(d0), cuuint64_t(d1), cuuint64_t(nb1), cuuint64_t(nb2)};
@@ -334,43 +426,83 @@ bool make_map(CUtensorMap* map, const GemmOperand& op, long long d0, long long d
   return r == CUDA_SUCCESS;
 }
 
-template <int BN, int AM, int BMn>
-cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const EpiParams& p,
-                     cudaStream_t s) {
-  using C = Cfg<BN>;
+// 4D map over the output (or residual) matrix: {N, M, nb1, nb2}, box 32 x 32;
+// fp32 tiles use SWIZZLE_128B (128-byte rows), bf16 tiles SWIZZLE_64B
+bool make_map_c(CUtensorMap* map, void* ptr, int fp32, long long N, long long M, long long ld,
+                long long bs1, long long bs2, int nb1, int nb2) {
+  const int es = fp32 ? 4 : 2;
+  cuuint64_t dims[4] = {cuuint64_t(N), cuuint64_t(M), cuuint64_t(nb1), cuuint64_t(nb2)};
+  cuuint64_t strides[3] = {cuuint64_t(ld * es), cuuint64_t((bs1 ? bs1 : 1) * es),
+                           cuuint64_t((bs2 ? bs2 : 1) * es)};
+  if (nb1 == 1) strides[1] = strides[0] * cuuint64_t(M);
+  if (nb2 == 1) strides[2] = strides[1] * cuuint64_t(nb1);
+  for (int i = 0; i < 3; ++i)
+    if (strides[i] % 16 || strides[i] == 0) return false;
+  if (reinterpret_cast<uintptr_t>(ptr) % 16) return false;
+  cuuint32_t box[4] = {32, 32, 1, 1};
+  cuuint32_t esd[4] = {1, 1, 1, 1};
+  CUresult r = g_encode(map, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                        4, ptr, dims, strides, box, esd, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        fp32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, int AM, int BMn, int CG>
+cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                     const CUtensorMap& mr, const EpiParams& p, cudaStream_t s) {
+  using C = Cfg<BN, CG>;
   static bool attr_done = false;
+  auto kern = gemm_kernel<BN, AM, BMn, CG>;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, AM, BMn>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(C::SMEM));
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
   int sms = g_sm_limit > 0 ? std::min(g_sm_limit, g_num_sms) : g_num_sms;
-  int grid = std::min(p.num_tiles, sms);
+  int grid = std::min(p.num_tiles * CG, (sms / CG) * CG);
   if (grid <= 0) return cudaSuccess;
-  gemm_kernel<BN, AM, BMn><<<grid, kThreads, C::SMEM, s>>>(ma, mb, p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mr, p);
 }
 
-template <int BN>
+template <int BN, int CG>
 cudaError_t dispatch_major(int am, int bm, const CUtensorMap& ma, const CUtensorMap& mb,
-                           const EpiParams& p, cudaStream_t s) {
-  if (!am && !bm) return launch_t<BN, 0, 0>(ma, mb, p, s);
-  if (!am && bm) return launch_t<BN, 0, 1>(ma, mb, p, s);
-  if (am && !bm) return launch_t<BN, 1, 0>(ma, mb, p, s);
-  return launch_t<BN, 1, 1>(ma, mb, p, s);
+                           const CUtensorMap& mc, const CUtensorMap& mr, const EpiParams& p,
+                           cudaStream_t s) {
+  if (!am && !bm) return launch_t<BN, 0, 0, CG>(ma, mb, mc, mr, p, s);
+  if (!am && bm) return launch_t<BN, 0, 1, CG>(ma, mb, mc, mr, p, s);
+  if (am && !bm) return launch_t<BN, 1, 0, CG>(ma, mb, mc, mr, p, s);
+  return launch_t<BN, 1, 1, CG>(ma, mb, mc, mr, p, s);
 }
 
 }  // namespace
 
 void gemm_set_sm_limit(int sms) { g_sm_limit = sms; }
+void gemm_force_cta_group(int cg) { g_force_cg = cg; }
 
 cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream) {
   cudaError_t e = load_encode();
   if (e != cudaSuccess) return e;
   if (d.M <= 0 || d.N <= 0) return cudaSuccess;
-  // tile width: 256 for wide outputs, 128 otherwise (fewer wasted columns on narrow N)
+  if (d.R && !d.c_fp32) return cudaErrorInvalidValue;
+  // tile width: 256 for wide outputs, 128 otherwise; CTA pairs when M fills 256 rows
   const int BN = d.N >= 256 ? 256 : 128;
+  int CG = d.M > 128 ? 2 : 1;
+  if (g_force_cg) CG = g_force_cg;
+  const int BNC = BN / CG;
   CUtensorMap ma, mb;
   bool ok;
   if (d.A.mn_major)
@@ -381,12 +513,11 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream) {
   if (d.B.mn_major)
     ok = make_map(&mb, d.B, d.N, d.K, d.nb1, d.nb2, 64, BK);
   else
-    ok = make_map(&mb, d.B, d.K, d.N, d.nb1, d.nb2, BK, BN);
+    ok = make_map(&mb, d.B, d.K, d.N, d.nb1, d.nb2, BK, BNC);
   if (!ok) return cudaErrorInvalidValue;
   EpiParams p;
   p.C = d.C;
   p.R = d.R;
-  if (d.R && !d.c_fp32) return cudaErrorInvalidValue;
   p.ldc = d.ldc;
   p.cbs1 = d.cbs1;
   p.cbs2 = d.cbs2;
@@ -399,11 +530,27 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream) {
   p.beta = d.beta;
   p.alpha = d.alpha;
   p.causal = d.causal;
-  p.m_tiles = (d.M + BM - 1) / BM;
+  const int TM = BM * CG;
+  p.m_tiles = (d.M + TM - 1) / TM;
   p.n_tiles = (d.N + BN - 1) / BN;
   p.num_tiles = p.m_tiles * p.n_tiles * d.nb1 * d.nb2;
-  if (BN == 256) return dispatch_major<256>(d.A.mn_major, d.B.mn_major, ma, mb, p, stream);
-  return dispatch_major<128>(d.A.mn_major, d.B.mn_major, ma, mb, p, stream);
+  if (d.beta && !d.c_fp32) return cudaErrorInvalidValue;
+  CUtensorMap mc, mr;
+  if (!make_map_c(&mc, d.C, d.c_fp32, d.N, d.M, d.ldc, d.cbs1, d.cbs2, d.nb1, d.nb2))
+    return cudaErrorInvalidValue;
+  if (d.R) {
+    if (!make_map_c(&mr, const_cast<float*>(d.R), 1, d.N, d.M, d.ldc, d.cbs1, d.cbs2, d.nb1, d.nb2))
+      return cudaErrorInvalidValue;
+  } else {
+    mr = mc;
+  }
+  const int am = d.A.mn_major, bmj = d.B.mn_major;
+  if (CG == 2) {
+    if (BN == 256) return dispatch_major<256, 2>(am, bmj, ma, mb, mc, mr, p, stream);
+    return dispatch_major<128, 2>(am, bmj, ma, mb, mc, mr, p, stream);
+  }
+  if (BN == 256) return dispatch_major<256, 1>(am, bmj, ma, mb, mc, mr, p, stream);
+  return dispatch_major<128, 1>(am, bmj, ma, mb, mc, mr, p, stream);
 }
 
 }  // namespace hexexec

@@ -52,7 +52,11 @@ __global__ void cast_kernel(const float* in, bf16* out, long long n) {
 }
 
 __global__ void tokens_kernel(int32_t* tok, long long ns, int S1, long long sample0,
-                              uint64_t seed, long long step, int vocab) {
+                              uint64_t seed, long long step, int vocab, const StepParams* sp) {
+  if (sp) {
+    if (!sp->gen_tokens) return;
+    step = sp->cur_step;
+  }
   long long n = ns * S1;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
@@ -417,7 +421,12 @@ __global__ void scale_kernel(float* g, long long n, float scale) {
 __global__ void adamw_kernel(float* __restrict__ p, bf16* __restrict__ p16, float* __restrict__ m,
                              float* __restrict__ v, const bf16* __restrict__ g16,
                              const float* __restrict__ g32, long long n, float gscale, float lr,
-                             float b1, float b2, float eps, float wd, float bc1, float bc2) {
+                             float b1, float b2, float eps, float wd, float bc1, float bc2,
+                             const StepParams* sp) {
+  if (sp) {
+    bc1 = sp->bc1;
+    bc2 = sp->bc2;
+  }
   // 4 elements per thread-iteration: float4 p/m/v, 8-byte bf16 grad / copy
   const long long n4 = n / 4;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
@@ -484,9 +493,24 @@ void k_cast_bf16(const float* in, bf16* out, long long n, cudaStream_t s) {
   if (n > 0) cast_kernel<<<ew_grid(n, 4), 256, 0, s>>>(in, out, n);
 }
 void k_gen_tokens(int32_t* tok, long long ns, int S, long long sample0, uint64_t seed,
-                  long long step, int vocab, cudaStream_t s) {
+                  long long step, int vocab, cudaStream_t s, const StepParams* sp) {
   long long n = ns * (S + 1);
-  if (n > 0) tokens_kernel<<<ew_grid(n, 1), 256, 0, s>>>(tok, ns, S + 1, sample0, seed, step, vocab);
+  if (n > 0)
+    tokens_kernel<<<ew_grid(n, 1), 256, 0, s>>>(tok, ns, S + 1, sample0, seed, step, vocab, sp);
+}
+
+__global__ void step_tick_kernel(StepParams* sp, float b1, float b2) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    long long s = sp->next_step;
+    sp->cur_step = s;
+    sp->next_step = s + 1;
+    sp->bc1 = 1.f - powf(b1, float(s + 1));
+    sp->bc2 = 1.f - powf(b2, float(s + 1));
+  }
+}
+
+void k_step_tick(StepParams* sp, float b1, float b2, cudaStream_t s) {
+  step_tick_kernel<<<1, 32, 0, s>>>(sp, b1, b2);
 }
 void k_embed_fwd(const int32_t* tok, const float* E, float* x, int M, int S, int H,
                  cudaStream_t s) {
@@ -560,10 +584,10 @@ void k_scale(float* g, long long n, float scale, cudaStream_t s) {
 }
 void k_adamw(float* p, bf16* p16, float* m, float* v, const bf16* g16, const float* g32,
              long long n, float gscale, float lr, float b1, float b2, float eps, float wd,
-             float bc1, float bc2, cudaStream_t s) {
+             float bc1, float bc2, cudaStream_t s, const StepParams* sp) {
   if (n > 0)
     adamw_kernel<<<ew_grid(n, 4), 256, 0, s>>>(p, p16, m, v, g16, g32, n, gscale, lr, b1, b2, eps,
-                                               wd, bc1, bc2);
+                                               wd, bc1, bc2, sp);
 }
 
 }  // namespace hexexec

@@ -38,13 +38,26 @@ __host__ __device__ inline float init_normal(uint64_t tensor_seed, uint64_t idx)
 }
 constexpr uint64_t kTokenTag = 0x746f6b656e73ULL;  // "tokens"
 
+// per-step scalars kept on the device so a captured CUDA graph replays the step
+// unchanged: step_tick (first node) advances next_step and derives the AdamW
+// bias corrections; gen_tokens is set by a host memset before each launch.
+struct StepParams {
+  long long next_step;
+  long long cur_step;
+  float bc1, bc2;
+  int gen_tokens;
+  int pad;
+};
+void k_step_tick(StepParams* sp, float b1, float b2, cudaStream_t s);
+
 void k_init_normal(float* master, bf16* copy, long long n, long long global_offset,
                    uint64_t tensor_seed, cudaStream_t s);
 void k_fill(float* p, bf16* copy, long long n, float v, cudaStream_t s);
 void k_cast_bf16(const float* in, bf16* out, long long n, cudaStream_t s);
 // tokens[i][p], i in [0, n_samples), p in [0, S]: sample id = sample0 + i
+// sp != null: step and the gen flag come from the device StepParams
 void k_gen_tokens(int32_t* tok, long long n_samples, int S, long long sample0, uint64_t seed,
-                  long long step, int vocab, cudaStream_t s);
+                  long long step, int vocab, cudaStream_t s, const StepParams* sp = nullptr);
 
 // x[m, :] = E[tok(m), :]  (tok row stride S+1)
 void k_embed_fwd(const int32_t* tok, const float* E, float* x, int M, int S, int H,
@@ -98,6 +111,6 @@ void k_scale(float* g, long long n, float scale, cudaStream_t s);
 // AdamW on an fp32 master shard; grad is bf16 (g16) or fp32 (g32) times gscale
 void k_adamw(float* p, bf16* p16, float* m, float* v, const bf16* g16, const float* g32,
              long long n, float gscale, float lr, float b1, float b2, float eps, float wd,
-             float bc1, float bc2, cudaStream_t s);
+             float bc1, float bc2, cudaStream_t s, const StepParams* sp = nullptr);
 
 }  // namespace hexexec

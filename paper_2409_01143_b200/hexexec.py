@@ -100,6 +100,9 @@ class Executor:
         err = L.errbuf()
         L.check(L.hexexec_sync(self._h, err, len(err)), err)
 
+    def set_profile(self, on: bool):
+        L.check(L.hexexec_set_profile(self._h, 1 if on else 0), None, "set_profile")
+
     def timer_start(self):
         err = L.errbuf()
         L.check(L.hexexec_timer(self._h, 0, None, err, len(err)), err)
