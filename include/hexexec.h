@@ -124,6 +124,15 @@ hexexec_status hexexec_k_gemm(int M, int N, int K, int nb1, int nb2, const void*
                               int64_t ldb, int64_t b_bs1, int64_t b_bs2, void* C, int64_t ldc,
                               int64_t c_bs1, int64_t c_bs2, int c_fp32, int beta, float alpha,
                               int causal, void* stream);
+/* fused causal attention over the head-interleaved QKV buffer [mb*S, nh*3*d]:
+ * out [mb*S, nh*d] bf16, lse [mb*nh, S] (log2 domain); backward writes
+ * dq/dk/dv into dqkv [mb*S, nh*3*d] (delta / dq_acc: fp32 scratch of
+ * mb*nh*S and mb*S*nh*d floats). */
+hexexec_status hexexec_k_attn_fwd(const void* qkv, void* out, float* lse, int S, int nh, int d,
+                                  int mb, float scale, void* stream);
+hexexec_status hexexec_k_attn_bwd(const void* qkv, const void* out, const void* dout,
+                                  const float* lse, float* delta, float* dq_acc, void* dqkv, int S,
+                                  int nh, int d, int mb, float scale, void* stream);
 hexexec_status hexexec_k_rmsnorm_fwd(const float* x, const void* y_bf16, float* xo,
                                      const float* g, void* out_bf16, float* rstd, int M, int H,
                                      float eps, void* stream);

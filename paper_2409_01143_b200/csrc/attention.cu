@@ -1,0 +1,782 @@
+// Fused causal attention (flash-style) for sm_100a.
+//
+// Forward CTA = one (sample, head, 128-query tile).  Warp roles (256 thr):
+//   warp 0  TMA producer: Q tile once, then K/V tiles into a 2-slot ring
+//   warp 1  MMA issuer:   S_j = Q K_j^T (TMEM, double-buffered), O_j = P_j V_j (TMEM)
+//   warp 2  TMEM allocator (512 columns: S0 | S1 | O)
+//   warps 4-7 softmax: one thread per query row; online max / sum in fp32,
+//            P_j written bf16 into swizzled smem as the A operand of O_j,
+//            O accumulated in registers (O = O*alpha + O_j), LSE saved.
+// The MMA of S_{j+1} overlaps the softmax of S_j.  Causality: only key tiles
+// j <= query tile are visited; the diagonal tile is masked per element.
+// Backward: see attn_bwd_kernel below.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cfloat>
+#include <mutex>
+
+#include "attention.h"
+#include "common.cuh"
+
+namespace hexexec {
+
+namespace {
+
+constexpr int T = 128;          // query / key tile
+constexpr int kThreads = 256;
+constexpr uint32_t ATOM = 16384;  // [128 rows][64 bf16] SWIZZLE_128B atom column block
+
+struct AttnParams {
+  __nv_bfloat16* out;
+  float* lse;
+  int S, nh, mb, ldo;
+  float scale_log2;
+};
+
+template <int D>
+struct FwdCfg {
+  static constexpr uint32_t TILE = T * D * 2;          // Q / K / V tile bytes
+  static constexpr uint32_t P_BYTES = T * T * 2;
+  static constexpr uint32_t SMEM = 1024 + TILE * 5 + P_BYTES + 256;
+};
+
+HX_DEVICE uint32_t idesc_bf16(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(a_mn) << 15) | (uint32_t(b_mn) << 16) |
+         (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+}
+
+// K-major operand made of 64-column atoms: k-step ks of 16 elements
+HX_DEVICE uint64_t kdesc(uint32_t base, int ks) {
+  return umma_desc_sw128(base + (ks / 4) * ATOM + (ks % 4) * 32, 16, 1024);
+}
+
+// MN-major operand staged as [64-row k block][n atoms of 64][64 k rows x 128 B]
+template <int NATOMS>
+HX_DEVICE uint64_t mndesc(uint32_t base, int ks) {
+  return umma_desc_sw128(base + (ks / 4) * (NATOMS * 8192) + (ks % 4) * 2048, 8192, 1024);
+}
+
+// byte offset of 16-byte chunk `kc` (8 bf16 along K) of row r in a K-major
+// SWIZZLE_128B operand made of 64-column atoms of [128 rows][128 B]
+HX_DEVICE uint32_t kchunk(int r, int kc) {
+  return uint32_t((kc / 8) * ATOM + r * 128 + (((kc % 8) ^ (r % 8)) * 16));
+}
+
+// 16-byte chunk q of row r in a [32 rows][128 B] SWIZZLE_128B TMA box
+HX_DEVICE uint32_t swz128(int r, int q) { return uint32_t(r * 128 + ((q ^ (r % 8)) * 16)); }
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
+  using C = FwdCfg<D>;
+  constexpr int DA = D / 64;  // 64-column atoms across the head dim
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + C::TILE;          // [2]
+  uint8_t* sV = sK + 2 * C::TILE;      // [2]
+  uint8_t* sP = sV + 2 * C::TILE;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + C::P_BYTES);
+  uint64_t* q_full = bar;
+  uint64_t* kv_full = bar + 1;   // [2]
+  uint64_t* kv_empty = bar + 3;  // [2]
+  uint64_t* s_full = bar + 5;    // [2]
+  uint64_t* s_empty = bar + 7;   // [2]
+  uint64_t* p_full = bar + 9;
+  uint64_t* o_full = bar + 10;
+  uint64_t* o_empty = bar + 11;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 12);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int nqt = p.S / T;
+  const int qt = nqt - 1 - int(blockIdx.x % nqt);  // heaviest query tiles first
+  const int zh = int(blockIdx.x / nqt);
+  const int h = zh % p.nh;
+  const int b = zh / p.nh;
+  const int ntiles = qt + 1;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 4);
+    }
+    mbar_init(p_full, 4);
+    mbar_init(o_full, 1);
+    mbar_init(o_empty, 4);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, C::TILE);
+      for (int a = 0; a < DA; ++a) tma_load_4d(sQ + a * ATOM, &tmQ, q_full, a * 64, qt * T, h, b);
+      for (int j = 0; j < ntiles; ++j) {
+        const int slot = j & 1;
+        mbar_wait(&kv_empty[slot], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[slot], 2 * C::TILE);
+        uint8_t* k = sK + slot * C::TILE;
+        uint8_t* v = sV + slot * C::TILE;
+        for (int a = 0; a < DA; ++a)
+          tma_load_4d(k + a * ATOM, &tmK, &kv_full[slot], a * 64, j * T, h, b);
+        for (int kb = 0; kb < 2; ++kb)
+          for (int a = 0; a < DA; ++a)
+            tma_load_4d(v + kb * (DA * 8192) + a * 8192, &tmV, &kv_full[slot], a * 64,
+                        j * T + kb * 64, h, b);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t id_s = idesc_bf16(T, T, 0, 0);
+      const uint32_t id_o = idesc_bf16(T, D, 0, 1);
+      const uint32_t q_addr = smem_u32(sQ);
+      const uint32_t p_addr = smem_u32(sP);
+      mbar_wait(q_full, 0);
+      auto issue_s = [&](int j) {
+        const int slot = j & 1;
+        mbar_wait(&kv_full[slot], (j >> 1) & 1);
+        mbar_wait(&s_empty[slot], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sK + slot * C::TILE);
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks)
+          tc_mma_f16(tbase + uint32_t(slot * T), kdesc(q_addr, ks), kdesc(k_addr, ks), id_s,
+                     ks > 0 ? 1u : 0u);
+        tc_commit(&s_full[slot]);
+      };
+      issue_s(0);
+      for (int j = 0; j < ntiles; ++j) {
+        const int slot = j & 1;
+        if (j + 1 < ntiles) issue_s(j + 1);
+        mbar_wait(p_full, j & 1);
+        tc_fence_after();
+        const uint32_t v_addr = smem_u32(sV + slot * C::TILE);
+        // O accumulates in TMEM across key tiles (rescaled in place by the
+        // softmax warps when their reference max moves)
+#pragma unroll
+        for (int ks = 0; ks < T / 16; ++ks)
+          tc_mma_f16(tbase + 2 * T, kdesc(p_addr, ks), mndesc<DA>(v_addr, ks), id_o,
+                     (j > 0 || ks > 0) ? 1u : 0u);
+        tc_commit(o_full);
+        tc_commit(&kv_empty[slot]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    const int r = ew * 32 + lane;  // query row within the tile
+    const uint32_t lane_off = uint32_t(ew * 32) << 16;
+    // m is a *reference* max: P = 2^(s*c - m) may exceed 1 by up to 2^8; O (in
+    // TMEM) and l are rescaled only when some row's max grows past m + 8
+    constexpr float kSlack = 8.f;
+    float m = -FLT_MAX, l = 0.f;
+    for (int j = 0; j < ntiles; ++j) {
+      const int slot = j & 1;
+      const bool diag = j == qt;
+      mbar_wait(&s_full[slot], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t sv[T];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t* v = sv + c * 32;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+              "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+              "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]),
+              "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+              "=r"(v[30]), "=r"(v[31])
+            : "r"(tbase + lane_off + uint32_t(slot * T + c * 32)));
+      }
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[slot]);  // S slot may be overwritten now
+      // 8 independent partial maxima (short dependency chains)
+      float mx[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mx[k] = -FLT_MAX;
+#pragma unroll
+      for (int i = 0; i < T; ++i)
+        if (!diag || i <= r) mx[i % 8] = fmaxf(mx[i % 8], __uint_as_float(sv[i]));
+      float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                       fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+      mt *= p.scale_log2;
+      // P buffer and O must be released by the previous PV MMA first
+      if (j > 0) {
+        mbar_wait(o_full, (j - 1) & 1);
+        tc_fence_after();
+      }
+      if (__any_sync(0xffffffffu, mt > m + kSlack)) {
+        const float m_new = fmaxf(m, mt);
+        const float alpha = ex2(m - m_new);
+        if (j > 0) {
+#pragma unroll 1
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(tbase + lane_off + uint32_t(2 * T + c * 32), v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+            tmem_st_32x32b_x32(tbase + lane_off + uint32_t(2 * T + c * 32), v);
+          }
+          tmem_st_wait();
+        }
+        l *= alpha;
+        m = m_new;
+      }
+      float lsp[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) lsp[k] = 0.f;
+#pragma unroll
+      for (int q = 0; q < T / 8; ++q) {
+        float pr[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int i = q * 8 + k;
+          const float e = ex2(fmaf(__uint_as_float(sv[i]), p.scale_log2, -m));
+          pr[k] = (!diag || i <= r) ? e : 0.f;
+          lsp[k] += pr[k];
+        }
+        uint4 w;
+        w.x = pack_bf16x2(pr[0], pr[1]);
+        w.y = pack_bf16x2(pr[2], pr[3]);
+        w.z = pack_bf16x2(pr[4], pr[5]);
+        w.w = pack_bf16x2(pr[6], pr[7]);
+        *reinterpret_cast<uint4*>(sP + kchunk(r, q)) = w;
+      }
+      l += ((lsp[0] + lsp[1]) + (lsp[2] + lsp[3])) + ((lsp[4] + lsp[5]) + (lsp[6] + lsp[7]));
+      tc_fence_before();
+      fence_async_shared();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    mbar_wait(o_full, (ntiles - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    const int qi = qt * T + r;
+    __nv_bfloat16* dst = p.out + ((long long)b * p.S + qi) * p.ldo + (long long)h * D;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tbase + lane_off + uint32_t(2 * T + c * 32), v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 w;
+        w.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]) * inv, __uint_as_float(v[8 * q + 1]) * inv);
+        w.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv);
+        w.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv);
+        w.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv);
+        reinterpret_cast<uint4*>(dst)[c * 4 + q] = w;
+      }
+    }
+    p.lse[((long long)b * p.nh + h) * p.S + qi] = m + log2f(l);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
+// ------------------------------------------------------------------ backward
+// CTA = one (sample, head, 128-key tile kt); loops over query tiles i >= kt.
+// Transposed formulation so TMEM rows are keys:
+//   S^T = K Q_i^T, dP^T = V dO_i^T                    (TMEM, fp32)
+//   P^T = exp2(S^T*scale_log2 - lse_q), dS^T = P^T (dP^T - delta_q) * scale
+//   dV += P^T dO_i, dK += dS^T Q_i                    (TMEM accumulators)
+//   dQ_i  = dS K  -> TMA reduce-add into an fp32 dq accumulator in HBM
+// P^T / dS^T share one bf16 smem buffer (K-major over queries); the same smem
+// tiles serve as MN-major operands (LBO = one 64-column atom).
+struct BwdParams {
+  float* dq_acc;
+  const float* lse;
+  const float* delta;
+  __nv_bfloat16* dqkv;
+  int S, nh, mb;
+  float scale, scale_log2;
+};
+
+template <int D>
+struct BwdCfg {
+  static constexpr uint32_t TILE = T * D * 2;
+  static constexpr uint32_t PDS = T * T * 2;
+  static constexpr uint32_t SMEM = 1024 + 6 * TILE + PDS + 2 * T * 4 + 256;
+};
+
+template <int NATOMS_UNUSED>
+HX_DEVICE uint64_t mnview(uint32_t base, int ks) {
+  // K-major tile [atom][128 rows][64] read as MN-major: k = rows, mn = columns
+  return umma_desc_sw128(base + ks * 2048, ATOM, 1024);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                    const __grid_constant__ CUtensorMap tmDQ, const BwdParams p) {
+  using C = BwdCfg<D>;
+  constexpr int DA = D / 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + C::TILE;
+  uint8_t* sQ = sV + C::TILE;          // [2]
+  uint8_t* sDO = sQ + 2 * C::TILE;     // [2]
+  uint8_t* sPD = sDO + 2 * C::TILE;    // P^T / dS^T / dQ staging
+  float* sLse = reinterpret_cast<float*>(sPD + C::PDS);
+  float* sDel = sLse + T;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sDel + T);
+  uint64_t* kv_full = bar;
+  uint64_t* qdo_full = bar + 1;    // [2]
+  uint64_t* qdo_empty = bar + 3;   // [2]
+  uint64_t* s_full = bar + 5;
+  uint64_t* dp_full = bar + 6;
+  uint64_t* p_full = bar + 7;
+  uint64_t* pds_free = bar + 8;
+  uint64_t* ds_full = bar + 9;
+  uint64_t* dq_full = bar + 10;
+  uint64_t* dq_empty = bar + 11;
+  uint64_t* dkv_full = bar + 12;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 13);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int nt = p.S / T;
+  const int kt = int(blockIdx.x % nt);  // small kt = most query tiles: launched first
+  const int zh = int(blockIdx.x / nt);
+  const int h = zh % p.nh;
+  const int b = zh / p.nh;
+  const int ntiles = nt - kt;
+  // TMEM columns: S^T / dQ [0,128) | dP^T [128,256) | dV [256,256+D) | dK [384, 384+D)
+  constexpr uint32_t cS = 0, cP = 128, cV = 256, cK = 384;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    tma_prefetch(&tmDO);
+    tma_prefetch(&tmDQ);
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&qdo_full[i], 1);
+      mbar_init(&qdo_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(dp_full, 1);
+    mbar_init(p_full, 4);
+    mbar_init(pds_free, 1);
+    mbar_init(ds_full, 4);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_empty, 4);
+    mbar_init(dkv_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(kv_full, 2 * C::TILE);
+      for (int a = 0; a < DA; ++a) {
+        tma_load_4d(sK + a * ATOM, &tmK, kv_full, a * 64, kt * T, h, b);
+        tma_load_4d(sV + a * ATOM, &tmV, kv_full, a * 64, kt * T, h, b);
+      }
+      for (int t = 0; t < ntiles; ++t) {
+        const int i = kt + t;
+        const int slot = t & 1;
+        mbar_wait(&qdo_empty[slot], ((t >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&qdo_full[slot], 2 * C::TILE);
+        for (int a = 0; a < DA; ++a) {
+          tma_load_4d(sQ + slot * C::TILE + a * ATOM, &tmQ, &qdo_full[slot], a * 64, i * T, h, b);
+          tma_load_4d(sDO + slot * C::TILE + a * ATOM, &tmDO, &qdo_full[slot], a * 64, i * T, h, b);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t id_sp = idesc_bf16(T, T, 0, 0);   // K-major x K-major, N = 128 queries
+      const uint32_t id_acc = idesc_bf16(T, D, 0, 1);  // A K-major, B MN-major, N = D
+      const uint32_t id_dq = idesc_bf16(T, D, 1, 1);   // A MN-major (dS view), B MN-major (K view)
+      const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), pd_addr = smem_u32(sPD);
+      mbar_wait(kv_full, 0);
+      for (int t = 0; t < ntiles; ++t) {
+        const int slot = t & 1;
+        const uint32_t q_addr = smem_u32(sQ + slot * C::TILE);
+        const uint32_t do_addr = smem_u32(sDO + slot * C::TILE);
+        mbar_wait(&qdo_full[slot], (t >> 1) & 1);
+        mbar_wait(dq_empty, (t & 1) ^ 1);  // S region (holds dQ_{t-1}) read out
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks)
+          tc_mma_f16(tbase + cS, kdesc(k_addr, ks), kdesc(q_addr, ks), id_sp, ks > 0 ? 1u : 0u);
+        tc_commit(s_full);
+        mbar_wait(ds_full, (t & 1) ^ 1);  // dP region (dP_{t-1}) consumed
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks)
+          tc_mma_f16(tbase + cP, kdesc(v_addr, ks), kdesc(do_addr, ks), id_sp, ks > 0 ? 1u : 0u);
+        tc_commit(dp_full);
+        mbar_wait(p_full, t & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < T / 16; ++ks)
+          tc_mma_f16(tbase + cV, kdesc(pd_addr, ks), mnview<0>(do_addr, ks), id_acc,
+                     (t > 0 || ks > 0) ? 1u : 0u);
+        tc_commit(pds_free);
+        mbar_wait(ds_full, t & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < T / 16; ++ks)
+          tc_mma_f16(tbase + cK, kdesc(pd_addr, ks), mnview<0>(q_addr, ks), id_acc,
+                     (t > 0 || ks > 0) ? 1u : 0u);
+#pragma unroll
+        for (int ks = 0; ks < T / 16; ++ks)
+          tc_mma_f16(tbase + cS, mnview<0>(pd_addr, ks), mnview<0>(k_addr, ks), id_dq,
+                     ks > 0 ? 1u : 0u);
+        tc_commit(dq_full);
+        tc_commit(&qdo_empty[slot]);
+      }
+      tc_commit(dkv_full);
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    const int tid = threadIdx.x - 128;          // 0..127
+    const int kr = ew * 32 + lane;              // key row within the tile (TMEM lane)
+    const uint32_t lane_off = uint32_t(ew * 32) << 16;
+    uint8_t* stage = sPD + ew * (32 * 64 * 4);  // dQ staging: [32 rows][64 fp32] per warp
+    for (int t = 0; t < ntiles; ++t) {
+      const int i = kt + t;
+      const bool diag = t == 0;
+      const long long zq = ((long long)b * p.nh + h) * p.S + (long long)i * T;
+      // per-query statistics of this tile, shared by the four warps
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      sLse[tid] = p.lse[zq + tid];
+      sDel[tid] = p.delta[zq + tid];
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      // P^T
+      mbar_wait(s_full, t & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tbase + lane_off + cS + uint32_t(c * 32), v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int q8 = 0; q8 < 4; ++q8) {
+          float pr[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int qc = c * 32 + q8 * 8 + k;
+            const float e = ex2(__uint_as_float(v[q8 * 8 + k]) * p.scale_log2 - sLse[qc]);
+            pr[k] = (diag && kr > qc) ? 0.f : e;
+          }
+          uint4 w;
+          w.x = pack_bf16x2(pr[0], pr[1]);
+          w.y = pack_bf16x2(pr[2], pr[3]);
+          w.z = pack_bf16x2(pr[4], pr[5]);
+          w.w = pack_bf16x2(pr[6], pr[7]);
+          *reinterpret_cast<uint4*>(sPD + kchunk(kr, c * 4 + q8)) = w;
+        }
+      }
+      fence_async_shared();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+      // dS^T (after dV has consumed P^T)
+      mbar_wait(dp_full, t & 1);
+      mbar_wait(pds_free, t & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t sv[32], dv[32];
+        tmem_ld_32x32b_x32(tbase + lane_off + cS + uint32_t(c * 32), sv);
+        tmem_ld_32x32b_x32(tbase + lane_off + cP + uint32_t(c * 32), dv);
+        tmem_ld_wait();
+#pragma unroll
+        for (int q8 = 0; q8 < 4; ++q8) {
+          float ds[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int qc = c * 32 + q8 * 8 + k;
+            const float pe = ex2(__uint_as_float(sv[q8 * 8 + k]) * p.scale_log2 - sLse[qc]);
+            const float pv = (diag && kr > qc) ? 0.f : pe;
+            ds[k] = pv * (__uint_as_float(dv[q8 * 8 + k]) - sDel[qc]) * p.scale;
+          }
+          uint4 w;
+          w.x = pack_bf16x2(ds[0], ds[1]);
+          w.y = pack_bf16x2(ds[2], ds[3]);
+          w.z = pack_bf16x2(ds[4], ds[5]);
+          w.w = pack_bf16x2(ds[6], ds[7]);
+          *reinterpret_cast<uint4*>(sPD + kchunk(kr, c * 4 + q8)) = w;
+        }
+      }
+      tc_fence_before();
+      fence_async_shared();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ds_full);
+      // dQ_i partial (TMEM rows = queries) -> staged fp32 -> TMA reduce-add
+      mbar_wait(dq_full, t & 1);
+      tc_fence_after();
+      const int qrow = i * T + ew * 32;  // first query row of this warp's slab
+#pragma unroll
+      for (int half = 0; half < D / 64; ++half) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(tbase + lane_off + cS + uint32_t(half * 64 + c * 32), v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<float4*>(stage + c * 4096 + swz128(lane, q)) =
+                make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                            __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+        }
+        fence_async_shared();
+        __syncwarp();
+        if (lane == 0) {
+          tma_reduce_add_4d(&tmDQ, stage, h * D + half * 64, b * p.S + qrow, 0, 0);
+          tma_reduce_add_4d(&tmDQ, stage + 4096, h * D + half * 64 + 32, b * p.S + qrow, 0, 0);
+          bulk_commit();
+          bulk_wait_read<0>();
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dq_empty);
+    }
+    // dK, dV of this key tile -> bf16 into the dqkv buffer
+    mbar_wait(dkv_full, 0);
+    tc_fence_after();
+    const long long row = (long long)b * p.S + kt * T + kr;
+    __nv_bfloat16* dst = p.dqkv + row * (3LL * p.nh * D) + (long long)h * 3 * D;
+#pragma unroll
+    for (int part = 0; part < 2; ++part) {
+      const uint32_t col0 = part == 0 ? cK : cV;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tbase + lane_off + col0 + uint32_t(c * 32), v);
+        tmem_ld_wait();
+        float f[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) f[k] = __uint_as_float(v[k]);
+        uint4* o = reinterpret_cast<uint4*>(dst + (part + 1) * D + c * 32);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 w;
+          w.x = pack_bf16x2(f[8 * q + 0], f[8 * q + 1]);
+          w.y = pack_bf16x2(f[8 * q + 2], f[8 * q + 3]);
+          w.z = pack_bf16x2(f[8 * q + 4], f[8 * q + 5]);
+          w.w = pack_bf16x2(f[8 * q + 6], f[8 * q + 7]);
+          o[q] = w;
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
+// delta[z][q] = sum_e dO[q, e] * O[q, e]  (thread per (row, head))
+template <int D>
+__global__ void attn_delta_kernel(const __nv_bfloat16* __restrict__ o,
+                                  const __nv_bfloat16* __restrict__ dout, float* delta, int S,
+                                  int nh, int mb) {
+  const long long n = (long long)mb * S * nh;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int h = int(idx % nh);
+    const long long row = idx / nh;  // b*S + s
+    const long long off = row * (long long)nh * D + (long long)h * D;
+    float acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < D / 8; ++c) {
+      uint4 a = reinterpret_cast<const uint4*>(o + off)[c];
+      uint4 g = reinterpret_cast<const uint4*>(dout + off)[c];
+      const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
+      const __nv_bfloat162* pg = reinterpret_cast<const __nv_bfloat162*>(&g);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        acc += __low2float(pa[k]) * __low2float(pg[k]) + __high2float(pa[k]) * __high2float(pg[k]);
+    }
+    const int bb = int(row / S), s = int(row % S);
+    delta[((long long)bb * nh + h) * S + s] = acc;
+  }
+}
+
+// dq (fp32 accumulator [M, nh*D]) -> bf16 q slots of dqkv [M, nh*3*D]
+template <int D>
+__global__ void attn_dq_cast_kernel(const float* __restrict__ dq, __nv_bfloat16* __restrict__ dqkv,
+                                    long long M, int nh) {
+  const long long n = M * nh * (D / 8);
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int c = int(idx % (D / 8));
+    const long long t = idx / (D / 8);
+    const int h = int(t % nh);
+    const long long row = t / nh;
+    const float4* src = reinterpret_cast<const float4*>(dq + row * nh * D + h * D + c * 8);
+    float4 a = src[0], bq = src[1];
+    uint4 w;
+    w.x = pack_bf16x2(a.x, a.y);
+    w.y = pack_bf16x2(a.z, a.w);
+    w.z = pack_bf16x2(bq.x, bq.y);
+    w.w = pack_bf16x2(bq.z, bq.w);
+    *reinterpret_cast<uint4*>(dqkv + row * 3LL * nh * D + (long long)h * 3 * D + c * 8) = w;
+  }
+}
+
+// ------------------------------------------------------------------ host
+PFN_cuTensorMapEncodeTiled_v12000 g_enc = nullptr;
+std::once_flag g_enc_once;
+
+// 4D bf16 map: element (e, s, h, b) at base + (b*S + s)*row_stride + h*head_stride + e
+bool encode(CUtensorMap* map, const void* base, int d, int S, int nh, int mb, long long row_stride,
+            long long head_stride, uint32_t box0, uint32_t box1) {
+  std::call_once(g_enc_once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!g_enc) return false;
+  cuuint64_t dims[4] = {cuuint64_t(d), cuuint64_t(S), cuuint64_t(nh), cuuint64_t(mb)};
+  cuuint64_t strides[3] = {cuuint64_t(row_stride * 2), cuuint64_t(head_stride * 2),
+                           cuuint64_t(row_stride * 2 * S)};
+  cuuint32_t box[4] = {box0, box1, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return g_enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
+               box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// fp32 [rows, cols] map, box 32 x 32, SWIZZLE_128B (dq accumulator, TMA reduce-add)
+bool encode_f32(CUtensorMap* map, float* base, long long cols, long long rows) {
+  cuuint64_t dims[4] = {cuuint64_t(cols), cuuint64_t(rows), 1, 1};
+  cuuint64_t strides[3] = {cuuint64_t(cols * 4), cuuint64_t(cols * 4 * rows),
+                           cuuint64_t(cols * 4 * rows)};
+  cuuint32_t box[4] = {32, 32, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return g_enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int D>
+cudaError_t launch_fwd(const AttnDesc& a, cudaStream_t s) {
+  using C = FwdCfg<D>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<D>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const long long W = 3LL * a.nh * D;
+  CUtensorMap q, k, v;
+  if (!encode(&q, a.qkv, D, a.S, a.nh, a.mb, W, 3 * D, 64, T) ||
+      !encode(&k, a.qkv + D, D, a.S, a.nh, a.mb, W, 3 * D, 64, T) ||
+      !encode(&v, a.qkv + 2 * D, D, a.S, a.nh, a.mb, W, 3 * D, 64, 64))
+    return cudaErrorInvalidValue;
+  AttnParams p;
+  p.out = a.out;
+  p.lse = a.lse;
+  p.S = a.S;
+  p.nh = a.nh;
+  p.mb = a.mb;
+  p.ldo = a.nh * D;
+  p.scale_log2 = a.scale * 1.4426950408889634f;
+  const int grid = (a.S / T) * a.nh * a.mb;
+  attn_fwd_kernel<D><<<grid, kThreads, C::SMEM, s>>>(q, k, v, p);
+  return cudaGetLastError();
+}
+
+int ew_blocks(long long n) {
+  long long b = (n + 255) / 256;
+  return int(b > 148 * 16 ? 148 * 16 : (b < 1 ? 1 : b));
+}
+
+template <int D>
+cudaError_t launch_bwd(const AttnBwdDesc& a, cudaStream_t s) {
+  using C = BwdCfg<D>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel<D>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const long long W = 3LL * a.nh * D;
+  const long long M = (long long)a.mb * a.S;
+  CUtensorMap q, k, v, dO, dq;
+  if (!encode(&q, a.qkv, D, a.S, a.nh, a.mb, W, 3 * D, 64, T) ||
+      !encode(&k, a.qkv + D, D, a.S, a.nh, a.mb, W, 3 * D, 64, T) ||
+      !encode(&v, a.qkv + 2 * D, D, a.S, a.nh, a.mb, W, 3 * D, 64, T) ||
+      !encode(&dO, a.dout, D, a.S, a.nh, a.mb, (long long)a.nh * D, D, 64, T) ||
+      !encode_f32(&dq, a.dq_acc, (long long)a.nh * D, M))
+    return cudaErrorInvalidValue;
+  cudaError_t e = cudaMemsetAsync(a.dq_acc, 0, size_t(M) * a.nh * D * sizeof(float), s);
+  if (e != cudaSuccess) return e;
+  attn_delta_kernel<D><<<ew_blocks(M * a.nh), 256, 0, s>>>(a.out, a.dout, a.delta, a.S, a.nh, a.mb);
+  BwdParams p;
+  p.dq_acc = a.dq_acc;
+  p.lse = a.lse;
+  p.delta = a.delta;
+  p.dqkv = a.dqkv;
+  p.S = a.S;
+  p.nh = a.nh;
+  p.mb = a.mb;
+  p.scale = a.scale;
+  p.scale_log2 = a.scale * 1.4426950408889634f;
+  const int grid = (a.S / T) * a.nh * a.mb;
+  attn_bwd_kernel<D><<<grid, kThreads, C::SMEM, s>>>(q, k, v, dO, dq, p);
+  attn_dq_cast_kernel<D><<<ew_blocks(M * a.nh * (D / 8)), 256, 0, s>>>(a.dq_acc, a.dqkv, M, a.nh);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t attention_fwd(const AttnDesc& a, cudaStream_t s) {
+  if (a.S % T != 0 || a.S <= 0) return cudaErrorInvalidValue;
+  if (a.d == 128) return launch_fwd<128>(a, s);
+  if (a.d == 64) return launch_fwd<64>(a, s);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t attention_bwd(const AttnBwdDesc& a, cudaStream_t s) {
+  if (a.S % T != 0 || a.S <= 0) return cudaErrorInvalidValue;
+  if (a.d == 128) return launch_bwd<128>(a, s);
+  if (a.d == 64) return launch_bwd<64>(a, s);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace hexexec

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <string>
 
+#include "attention.h"
 #include "executor.hpp"
 #include "gemm.h"
 #include "kernels.h"
@@ -276,6 +277,39 @@ hexexec_status hexexec_k_gemm(int M, int N, int K, int nb1, int nb2, const void*
   d.alpha = alpha;
   d.causal = causal;
   return cuda_status(hexexec::gemm_bf16(d, as_stream(stream)));
+}
+
+hexexec_status hexexec_k_attn_fwd(const void* qkv, void* out, float* lse, int S, int nh, int d,
+                                  int mb, float scale, void* stream) {
+  hexexec::AttnDesc a;
+  a.qkv = static_cast<const __nv_bfloat16*>(qkv);
+  a.out = static_cast<__nv_bfloat16*>(out);
+  a.lse = lse;
+  a.S = S;
+  a.nh = nh;
+  a.d = d;
+  a.mb = mb;
+  a.scale = scale;
+  return cuda_status(hexexec::attention_fwd(a, as_stream(stream)));
+}
+
+hexexec_status hexexec_k_attn_bwd(const void* qkv, const void* out, const void* dout,
+                                  const float* lse, float* delta, float* dq_acc, void* dqkv, int S,
+                                  int nh, int d, int mb, float scale, void* stream) {
+  hexexec::AttnBwdDesc a;
+  a.qkv = static_cast<const __nv_bfloat16*>(qkv);
+  a.out = static_cast<const __nv_bfloat16*>(out);
+  a.dout = static_cast<const __nv_bfloat16*>(dout);
+  a.lse = lse;
+  a.delta = delta;
+  a.dq_acc = dq_acc;
+  a.dqkv = static_cast<__nv_bfloat16*>(dqkv);
+  a.S = S;
+  a.nh = nh;
+  a.d = d;
+  a.mb = mb;
+  a.scale = scale;
+  return cuda_status(hexexec::attention_bwd(a, as_stream(stream)));
 }
 
 hexexec_status hexexec_k_rmsnorm_fwd(const float* x, const void* y, float* xo, const float* g,

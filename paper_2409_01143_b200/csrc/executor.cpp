@@ -28,6 +28,7 @@
 #include <map>
 #include <sstream>
 
+#include "attention.h"
 #include "gemm.h"
 #include "kernels.h"
 #include "nlohmann/json.hpp"
@@ -70,6 +71,7 @@ ExecConfig parse_exec_config(const std::string& text) {
       else if (k == "validate_only") c.validate_only = v.get<bool>();
       else if (k == "profile_gemm") c.profile_gemm = v.get<bool>();
       else if (k == "cuda_graph") c.cuda_graph = v.get<bool>();
+      else if (k == "attention") c.attention = v.get<std::string>();
       else throw ParseError("exec config: unknown key '" + k + "'");
     } catch (const nlohmann::json::exception& e) {
       throw ParseError("exec config: bad value for '" + k + "'");
@@ -77,6 +79,8 @@ ExecConfig parse_exec_config(const std::string& text) {
   }
   if (c.sm_cap != "green" && c.sm_cap != "cta" && c.sm_cap != "none")
     throw ParseError("exec config: sm_cap must be green|cta|none");
+  if (c.attention != "fused" && c.attention != "unfused")
+    throw ParseError("exec config: attention must be fused|unfused");
   if (c.dp_comm_dtype != "bf16" && c.dp_comm_dtype != "fp32")
     throw ParseError("exec config: dp_comm_dtype must be bf16|fp32");
   return c;
@@ -116,7 +120,8 @@ struct LayerActs {
   bf16* xn;         // [M, H]
   float* rstd1;     // [M]
   bf16* qkv;        // [M, 3 d nh]
-  bf16* P;          // [mb * nh, S, S]
+  bf16* P;          // [mb * nh, S, S]  (unfused attention only)
+  float* lse;       // [mb * nh, S]     (fused attention)
   bf16* attn;       // [M, d nh]
   bf16* hn;         // [M, H]
   float* rstd2;     // [M]
@@ -180,6 +185,7 @@ class Executor {
   float *dx[2] = {nullptr, nullptr}, *ce_scr = nullptr, *loss_acc = nullptr, *loss_host = nullptr;
   bf16* dxb = nullptr;
   float* coef_ = nullptr;
+  float *delta_ = nullptr, *dq_acc_ = nullptr;
   int32_t* tokens = nullptr;
   int32_t* tokens_pinned = nullptr;
   float* idle_loss_ = nullptr;
@@ -367,7 +373,11 @@ class Executor {
     const bool need_g16 = !L.dp_buckets[size_t(rank)].empty() && cfg.dp_comm_dtype == "bf16";
     n_slots = int(std::min<int64_t>(role.n_mb, role.stage_count - role.stage));
     n_slots = std::max(n_slots, 1);
-    const int64_t SS = mb * nh * S * S;
+    // unfused attention keeps S x S probabilities per (sample, head); the fused
+    // kernels keep only the per-row log-sum-exp
+    const bool fused = cfg.attention == "fused";
+    const int64_t SS = fused ? 0 : mb * nh * S * S;
+    const int64_t LSE = mb * nh * S;
     // parameters
     arena.reserve(P * 4 * 4);            // P32, G32, M, V
     arena.reserve(P * 2);                // P16
@@ -380,7 +390,8 @@ class Executor {
         arena.reserve(M * H * 2 * 2);              // xn, hn
         arena.reserve(M * 4 * 2);                  // rstd1, rstd2
         arena.reserve(M * qkvw * 2);               // qkv
-        arena.reserve(SS * 2);                     // P
+        arena.reserve(SS * 2);                     // P (unfused)
+        arena.reserve(LSE * 4);                    // lse (fused)
         arena.reserve(M * kr * 2);                 // attn
         arena.reserve(M * 2 * F * 2 + M * F * 2);  // gu, act
       }
@@ -392,6 +403,7 @@ class Executor {
     // scratch
     arena.reserve(SS * 4 * 2);  // scores, dP
     arena.reserve(SS * 2);      // dS
+    arena.reserve(LSE * 4 + M * kr * 4);  // fused bwd: delta, fp32 dq accumulator
     arena.reserve(M * H * 2);   // ypart
     arena.reserve(M * F * 2 + M * 2 * F * 2 + M * kr * 2 + M * qkvw * 2);
     arena.reserve(M * H * 4 * 2 + M * H * 2 + M * H * 2);  // dx ping-pong, dxb, dy16
@@ -419,6 +431,7 @@ class Executor {
         a.rstd2 = arena.take<float>(M);
         a.qkv = arena.take<bf16>(M * qkvw);
         a.P = arena.take<bf16>(SS);
+        a.lse = arena.take<float>(LSE);
         a.attn = arena.take<bf16>(M * kr);
         a.gu = arena.take<bf16>(M * 2 * F);
         a.act = arena.take<bf16>(M * F);
@@ -433,6 +446,8 @@ class Executor {
     scores = arena.take<float>(SS);
     dP = arena.take<float>(SS);
     dS = arena.take<bf16>(SS);
+    delta_ = arena.take<float>(LSE);
+    dq_acc_ = arena.take<float>(M * kr);
     ypart = arena.take<bf16>(M * H);
     da = arena.take<bf16>(M * F);
     dgu = arena.take<bf16>(M * 2 * F);
@@ -679,6 +694,21 @@ class Executor {
   // per (sample b, head h): scores = q k^T / sqrt(d) (causal tiles), P = softmax,
   // attn = P v -- batched over z = h + nh * b straight out of the QKV buffer
   void attention_fwd(LayerActs& a) {
+    if (cfg.attention == "fused") {
+      AttnDesc ad;
+      ad.qkv = a.qkv;
+      ad.out = a.attn;
+      ad.lse = a.lse;
+      ad.S = int(S);
+      ad.nh = int(nh);
+      ad.d = int(d);
+      ad.mb = int(mb);
+      ad.scale = 1.f / std::sqrt(float(d));
+      cudaError_t e = hexexec::attention_fwd(ad, stream);
+      if (e != cudaSuccess) throw CudaError(std::string("attention_fwd: ") + cudaGetErrorString(e));
+      kcheck("attn_fwd");
+      return;
+    }
     gemm_kind_ = 1;
     const int64_t SS2 = S * S;
     GemmDesc g;
@@ -805,6 +835,26 @@ class Executor {
   }
 
   void attention_bwd(LayerActs& a) {
+    if (cfg.attention == "fused") {
+      AttnBwdDesc ad;
+      ad.qkv = a.qkv;
+      ad.out = a.attn;
+      ad.dout = dattn;
+      ad.lse = a.lse;
+      ad.delta = delta_;
+      ad.dq_acc = dq_acc_;
+      ad.dqkv = dqkv;
+      ad.S = int(S);
+      ad.nh = int(nh);
+      ad.d = int(d);
+      ad.mb = int(mb);
+      ad.scale = 1.f / std::sqrt(float(d));
+      cudaError_t e = hexexec::attention_bwd(ad, stream);
+      if (e != cudaSuccess) throw CudaError(std::string("attention_bwd: ") + cudaGetErrorString(e));
+      launches_step += 2;  // delta + dq cast kernels (+ the main kernel below)
+      kcheck("attn_bwd");
+      return;
+    }
     gemm_kind_ = 1;
     const int64_t SS2 = S * S;
     // dP = dO V^T

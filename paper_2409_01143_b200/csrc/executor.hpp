@@ -19,6 +19,7 @@ struct ExecConfig {
   bool validate_only = false;
   bool profile_gemm = false;          // per-GEMM CUDA events (roofline evidence); eager
   bool cuda_graph = true;             // replay the captured step graph (after step 0)
+  std::string attention = "fused";    // "fused" (flash, tcgen05) | "unfused" (GEMM+softmax)
 };
 
 ExecConfig parse_exec_config(const std::string& text);

@@ -223,30 +223,56 @@ __global__ void rmsnorm_bwd_dx_kernel(const bf16* __restrict__ dyb, const float*
 
 // ------------------------------------------------------------------ rope
 // thread per (row, head, i < d/2) pair, applied to q and k
+__device__ __forceinline__ void unpack8(uint4 w, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    f[2 * k] = __low2float(h[k]);
+    f[2 * k + 1] = __high2float(h[k]);
+  }
+}
+
+__device__ __forceinline__ uint4 pack8(const float* f) {
+  uint4 w;
+  w.x = pack_bf16x2(f[0], f[1]);
+  w.y = pack_bf16x2(f[2], f[3]);
+  w.z = pack_bf16x2(f[4], f[5]);
+  w.w = pack_bf16x2(f[6], f[7]);
+  return w;
+}
+
+// thread per (row, head, q|k, 8 rotation pairs): 16-byte loads of both halves
 __global__ void rope_kernel(bf16* qkv, int M, int S, int nh, int d, float theta, int inverse) {
   const int half = d / 2;
-  long long n = (long long)M * nh * half;
+  const int g8 = half / 8;
+  const float l2t = log2f(theta);
+  long long n = (long long)M * nh * 2 * g8;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
        idx += (long long)gridDim.x * blockDim.x) {
-    int i = int(idx % half);
-    long long t = idx / half;
-    int h = int(t % nh);
-    int row = int(t / nh);
-    int pos = row % S;
-    float inv_freq = powf(theta, -2.0f * float(i) / float(d));
-    float ang = float(pos) * inv_freq;
-    float sn, cs;
-    sincosf(ang, &sn, &cs);
-    if (inverse) sn = -sn;
-    bf16* base = qkv + (long long)row * nh * 3 * d + (long long)h * 3 * d;
+    const int i8 = int(idx % g8);
+    long long t = idx / g8;
+    const int part = int(t % 2);
+    t /= 2;
+    const int h = int(t % nh);
+    const int row = int(t / nh);
+    const float pos = float(row % S);
+    bf16* base = qkv + (long long)row * nh * 3 * d + (long long)h * 3 * d + part * d + i8 * 8;
+    float a[8], b[8];
+    unpack8(*reinterpret_cast<const uint4*>(base), a);
+    unpack8(*reinterpret_cast<const uint4*>(base + half), b);
 #pragma unroll
-    for (int part = 0; part < 2; ++part) {
-      bf16* v = base + part * d;
-      float a = bf(v[i]);
-      float b = bf(v[i + half]);
-      v[i] = __float2bfloat16_rn(a * cs - b * sn);
-      v[i + half] = __float2bfloat16_rn(b * cs + a * sn);
+    for (int k = 0; k < 8; ++k) {
+      const int i = i8 * 8 + k;
+      const float inv_freq = exp2f(-2.0f * float(i) / float(d) * l2t);
+      float sn, cs;
+      sincosf(pos * inv_freq, &sn, &cs);
+      if (inverse) sn = -sn;
+      const float x = a[k], y = b[k];
+      a[k] = x * cs - y * sn;
+      b[k] = y * cs + x * sn;
     }
+    *reinterpret_cast<uint4*>(base) = pack8(a);
+    *reinterpret_cast<uint4*>(base + half) = pack8(b);
   }
 }
 
@@ -294,35 +320,44 @@ __global__ void softmax_bwd_kernel(const bf16* __restrict__ P, const float* __re
 // ------------------------------------------------------------------ swiglu
 __device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + __expf(-x)); }
 
+// thread per 8 consecutive ffn columns: 16-byte gate / up / out accesses
 __global__ void swiglu_fwd_kernel(const bf16* __restrict__ gu, bf16* __restrict__ a, int M,
                                   int F) {
-  long long n = (long long)M * F;
+  const long long n = (long long)M * (F / 8);
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
        idx += (long long)gridDim.x * blockDim.x) {
-    long long row = idx / F;
-    int f = int(idx % F);
-    int c = f / 64, j = f % 64;
-    const bf16* r = gu + row * 2 * F + c * 128;
-    float g = bf(r[j]), u = bf(r[64 + j]);
-    a[idx] = __float2bfloat16_rn(g * sigmoidf_(g) * u);
+    const long long row = idx / (F / 8);
+    const int f = int(idx % (F / 8)) * 8;
+    const bf16* r = gu + row * 2 * F + (f / 64) * 128 + (f % 64);
+    float g[8], u[8], o[8];
+    unpack8(*reinterpret_cast<const uint4*>(r), g);
+    unpack8(*reinterpret_cast<const uint4*>(r + 64), u);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = g[k] * sigmoidf_(g[k]) * u[k];
+    *reinterpret_cast<uint4*>(a + row * F + f) = pack8(o);
   }
 }
 
 __global__ void swiglu_bwd_kernel(const bf16* __restrict__ gu, const bf16* __restrict__ da,
                                   bf16* __restrict__ dgu, int M, int F) {
-  long long n = (long long)M * F;
+  const long long n = (long long)M * (F / 8);
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
        idx += (long long)gridDim.x * blockDim.x) {
-    long long row = idx / F;
-    int f = int(idx % F);
-    int c = f / 64, j = f % 64;
-    long long off = row * 2 * F + c * 128;
-    float g = bf(gu[off + j]), u = bf(gu[off + 64 + j]);
-    float d = bf(da[idx]);
-    float sg = sigmoidf_(g);
-    float silu = g * sg;
-    dgu[off + j] = __float2bfloat16_rn(d * u * sg * (1.f + g * (1.f - sg)));
-    dgu[off + 64 + j] = __float2bfloat16_rn(d * silu);
+    const long long row = idx / (F / 8);
+    const int f = int(idx % (F / 8)) * 8;
+    const long long off = row * 2 * F + (f / 64) * 128 + (f % 64);
+    float g[8], u[8], d[8], dg[8], du[8];
+    unpack8(*reinterpret_cast<const uint4*>(gu + off), g);
+    unpack8(*reinterpret_cast<const uint4*>(gu + off + 64), u);
+    unpack8(*reinterpret_cast<const uint4*>(da + row * F + f), d);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float sg = sigmoidf_(g[k]);
+      dg[k] = d[k] * u[k] * sg * (1.f + g[k] * (1.f - sg));
+      du[k] = d[k] * g[k] * sg;
+    }
+    *reinterpret_cast<uint4*>(dgu + off) = pack8(dg);
+    *reinterpret_cast<uint4*>(dgu + off + 64) = pack8(du);
   }
 }
 
@@ -531,7 +566,7 @@ void k_rmsnorm_bwd(const bf16* dyb, const float* dyf, const float* x, const floa
                    const float* g, const float* dres, float* dx, bf16* dxb, float* dg, int M,
                    int H, float* coef, cudaStream_t s) {
   if (M <= 0) return;
-  const int band = 64;
+  const int band = 16;  // rows per block: enough blocks in flight to cover HBM latency
   dim3 g2((H / 4 + 127) / 128, (M + band - 1) / band);
   if (dyb) {
     rmsnorm_bwd_dot_kernel<true><<<row_grid(M, 8), 256, 0, s>>>(dyb, dyf, x, rstd, g, coef, M, H);
@@ -543,7 +578,7 @@ void k_rmsnorm_bwd(const bf16* dyb, const float* dyf, const float* x, const floa
 }
 void k_rope(bf16* qkv, int M, int S, int nh, int d, float theta, int inverse, cudaStream_t s) {
   long long n = (long long)M * nh * (d / 2);
-  if (n > 0) rope_kernel<<<ew_grid(n, 1), 256, 0, s>>>(qkv, M, S, nh, d, theta, inverse);
+  if (n > 0) rope_kernel<<<ew_grid(n, 4), 256, 0, s>>>(qkv, M, S, nh, d, theta, inverse);
 }
 void k_softmax_fwd(const float* S, bf16* P, int L, int nb, cudaStream_t s) {
   long long rows = (long long)L * nb;
@@ -556,11 +591,11 @@ void k_softmax_bwd(const bf16* P, const float* dP, bf16* dS, float scale, int L,
 }
 void k_swiglu_fwd(const bf16* gu, bf16* a, int M, int F, cudaStream_t s) {
   long long n = (long long)M * F;
-  if (n > 0) swiglu_fwd_kernel<<<ew_grid(n, 2), 256, 0, s>>>(gu, a, M, F);
+  if (n > 0) swiglu_fwd_kernel<<<ew_grid(n, 8), 256, 0, s>>>(gu, a, M, F);
 }
 void k_swiglu_bwd(const bf16* gu, const bf16* da, bf16* dgu, int M, int F, cudaStream_t s) {
   long long n = (long long)M * F;
-  if (n > 0) swiglu_bwd_kernel<<<ew_grid(n, 2), 256, 0, s>>>(gu, da, dgu, M, F);
+  if (n > 0) swiglu_bwd_kernel<<<ew_grid(n, 8), 256, 0, s>>>(gu, da, dgu, M, F);
 }
 void k_ce_stats(const float* logits, int Vr, int v0, const int32_t* tok, int M, int S,
                 float* lmax, float* lsum, float* st2, cudaStream_t s) {

@@ -1,0 +1,49 @@
+"""Time the fused causal attention kernels at the Llama-7B shard shape."""
+import json
+import math
+import sys
+
+import torch
+
+sys.path.insert(0, __file__.rsplit("/scripts/", 1)[0])
+from paper_2409_01143_b200 import _lib as L  # noqa: E402
+
+
+def main(mb=1, S=2048, nh=32, d=128, iters=10):
+    torch.manual_seed(0)
+    qkv = torch.randn(mb * S, nh * 3 * d, device="cuda").bfloat16()
+    out = torch.zeros(mb * S, nh * d, device="cuda", dtype=torch.bfloat16)
+    lse = torch.zeros(mb * nh, S, device="cuda")
+    dout = torch.randn(mb * S, nh * d, device="cuda").bfloat16()
+    delta = torch.zeros(mb * nh, S, device="cuda")
+    dq = torch.zeros(mb * S, nh * d, device="cuda")
+    dqkv = torch.zeros_like(qkv)
+    sc = 1.0 / math.sqrt(d)
+
+    def fwd():
+        assert L.hexexec_k_attn_fwd(qkv.data_ptr(), out.data_ptr(), lse.data_ptr(), S, nh, d, mb,
+                                    sc, None) == 0
+
+    def bwd():
+        assert L.hexexec_k_attn_bwd(qkv.data_ptr(), out.data_ptr(), dout.data_ptr(),
+                                    lse.data_ptr(), delta.data_ptr(), dq.data_ptr(),
+                                    dqkv.data_ptr(), S, nh, d, mb, sc, None) == 0
+    res = {}
+    flops = 2.0 * 2 * mb * nh * S * S * d / 2  # causal fwd: QK^T + PV, lower triangle
+    for name, fn, f in (("fwd", fwd, flops), ("bwd", bwd, 2.5 * flops)):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(iters):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / iters
+        res[name] = {"ms": round(ms, 4), "tflops": round(f / ms / 1e9, 1)}
+    print(json.dumps({"shape": [mb, S, nh, d], **res}))
+
+
+if __name__ == "__main__":
+    main()

@@ -93,8 +93,9 @@ def check_against_oracle(name, ranks):
     assert seen == set(G), set(G) - seen  # every tensor is held somewhere
 
 
-def test_tiny_single_gpu(tmp_path):
-    ranks = run_plan("tiny_1", tmp_path, steps=3)
+@pytest.mark.parametrize("attention", ["fused", "unfused"])
+def test_tiny_single_gpu(tmp_path, attention):
+    ranks = run_plan("tiny_1", tmp_path, steps=3, xcfg={"attention": attention})
     check_against_oracle("tiny_1", ranks)
     l = ranks[0]["losses"]
     assert np.all(np.isfinite(l))
