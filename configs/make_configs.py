@@ -94,6 +94,8 @@ HAND = {
     "tiny_mixed4": ("b200_4_tiers", "tiny", plan([
         pipe(5, 1, [stage(["g0", "g2"], 0, 3, [2, 1]), stage(["g3"], 3, 1)]),
         pipe(3, 1, [stage(["g1"], 0, 4)])], 4)),
+    "tiny_pp3_4": ("b200_4_tiers", "tiny", plan([pipe(8, 2, [
+        stage(["g0"], 0, 2), stage(["g2", "g3"], 2, 1, [1, 3]), stage(["g1"], 3, 1)])], 4)),
     # N=1 workload: the cfg2 model on one B200
     "llama7b_4l_1gpu": ("b200_1", "llama7b_4l", plan([pipe(8, 1, [stage(["g0"], 0, 4)])], 4)),
     # cfg2: Llama-7B 4-layer block, TP=2 with 3:1 widths, rank 1 capped to 1/3 SMs

@@ -117,3 +117,8 @@ def test_tiny_two_rank_plans(tmp_path, name):
 
 def test_tiny_mixed_four_ranks(tmp_path):
     check_against_oracle("tiny_mixed4", run_plan("tiny_mixed4", tmp_path))
+
+
+def test_tiny_three_stage_pipeline_four_ranks(tmp_path):
+    # 3-stage 1F1B, TP=2 (widths 1:3) in the middle stage, TP degree changes at both hops
+    check_against_oracle("tiny_pp3_4", run_plan("tiny_pp3_4", tmp_path))
