@@ -93,7 +93,14 @@ class Arena {
  public:
   void reserve(size_t bytes) { total_ += align(bytes); }
   void commit() {
-    if (total_) HX_CUDA(cudaMalloc(&base_, total_));
+    if (!total_) return;
+    cudaError_t e = cudaMalloc(&base_, total_);
+    if (e == cudaErrorMemoryAllocation) {
+      (void)cudaGetLastError();
+      throw Infeasible("plan does not fit this device: rank needs " +
+                       std::to_string(total_ >> 20) + " MiB of HBM");
+    }
+    HX_CUDA(e);
   }
   template <typename T>
   T* take(size_t count) {
@@ -262,7 +269,11 @@ class Executor {
       qkvw = 3 * d * nh;
       kr = d * nh;
     }
-    if (cfg.validate_only) return;
+    if (cfg.validate_only) {
+      // host-only dry run: size the per-rank arena (no device needed)
+      if (role.active) allocate();
+      return;
+    }
 
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -411,6 +422,7 @@ class Executor {
     if (role.last_stage) arena.reserve(M * Vr * 4 + 5 * M * 4);
     arena.reserve(256);                                    // loss
     arena.reserve(role.batch * (S + 1) * 4);               // tokens
+    if (cfg.validate_only) return;
     arena.commit();
 
     P32 = arena.take<float>(P);
