@@ -140,14 +140,31 @@ def gather_sum(vals: list, rank: int, world: int, tag: str) -> list:
     return [sum(v[i] for v in allv) for i in range(len(vals))]
 
 
+def log(rank: int, msg: str):
+    print(f"[bench rank {rank} {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
 def run_plan(name: str, steps: int, warmup: int, rank: int, world: int, clocks: bool):
     from paper_2409_01143_b200 import dist
     c, m, p, idx = load(name)
+    log(rank, f"{name}: creating executor")
     ex = dist.make_executor(c, m, p, {}, tag=f"uid-{name}")
     role = ex.role
-    for _ in range(warmup):      # step 0 eager, step 1 captured into the CUDA graph
+    # ---- profiled pass first (eager, CUDA events around every GEMM and after every
+    # op): roofline evidence for the TP GEMMs + per-kernel-class step timeline.
+    # Eager NCCL work is kept before the first graph capture (no graph/eager mixing).
+    log(rank, f"{name}: profiled pass")
+    ex.set_profile(True)
+    for _ in range(2):
         ex.step_async()
     ex.sync()
+    st = ex.stats()
+    ex.set_profile(False)
+    log(rank, f"{name}: warm-up {warmup}")
+    for _ in range(warmup):      # first graph-mode step is captured into the CUDA graph
+        ex.step_async()
+    ex.sync()
+    log(rank, f"{name}: timed {steps}")
     # ---- device-timed region (tokens resident in HBM)
     dist.barrier(rank, world, f"t0-{name}")
     ck = Clocks() if clocks else None
@@ -161,6 +178,7 @@ def run_plan(name: str, steps: int, warmup: int, rank: int, world: int, clocks: 
     launches_step = ex.stats().get("launches_last_step", 0)
     dev_ms = gather_max([dev_ms], rank, world, f"dev-{name}")[0]
     # ---- e2e region: public API with host token buffers (H2D) + loss (D2H)
+    log(rank, f"{name}: e2e {steps}")
     toks = [ex.synth_tokens(warmup + steps + s) if role["active"] else None for s in range(steps)]
     dist.barrier(rank, world, f"e0-{name}")
     t0 = time.perf_counter()
@@ -170,15 +188,6 @@ def run_plan(name: str, steps: int, warmup: int, rank: int, world: int, clocks: 
     e2e_ms = (time.perf_counter() - t0) * 1e3
     e2e_ms = gather_max([e2e_ms], rank, world, f"e2e-{name}")[0]
     h2d = toks[0].nbytes if (role["active"] and toks[0] is not None) else 0
-    # ---- profiled pass (eager, CUDA events around every GEMM and after every op):
-    # roofline evidence for the TP GEMMs + per-kernel-class step timeline
-    ex.set_profile(True)
-    dist.barrier(rank, world, f"p0-{name}")
-    for _ in range(max(1, min(steps, 2))):
-        ex.step_async()
-    ex.sync()
-    st = ex.stats()
-    ex.set_profile(False)
     gp = st.get("gemm_profile", {})
     lin = gp.get("tp_linear", {})
     sums = gather_sum([float(h2d), 4.0, float(launches_step),
@@ -188,6 +197,7 @@ def run_plan(name: str, steps: int, warmup: int, rank: int, world: int, clocks: 
                        if role["active"] else 0.0],
                       rank, world, f"sum-{name}")
     ex.close()
+    log(rank, f"{name}: done")
     return dict(name=name, idx=idx, cluster=json.loads(c), model=json.loads(m),
                 plan=json.loads(p), dev_ms=dev_ms, e2e_ms=e2e_ms, loss=loss, clocks=clk,
                 stats=st, h2d=sums[0], d2h=sums[1], launches=sums[2], lin_flops=sums[3],

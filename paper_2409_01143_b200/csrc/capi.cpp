@@ -192,8 +192,7 @@ hexexec_status hexexec_sync(hexexec_ctx* ctx, char* err, size_t err_len) {
 
 hexexec_status hexexec_set_profile(hexexec_ctx* ctx, int on) {
   if (!ctx || !ctx->ex) return HEXEXEC_ERR_INVALID;
-  hexexec::executor_set_profile(*ctx->ex, on != 0);
-  return HEXEXEC_OK;
+  return guarded(nullptr, 0, [&] { hexexec::executor_set_profile(*ctx->ex, on != 0); });
 }
 
 hexexec_status hexexec_timer(hexexec_ctx* ctx, int stop, float* ms_out, char* err,

@@ -210,6 +210,15 @@ class Executor {
   ~Executor() { teardown(); }
 
   void teardown() {
+    // drain the stream and drop the captured graph (it holds NCCL persistent
+    // work) before the communicators: destroying a communicator still
+    // referenced by a graph exec blocks
+    if (stream) cudaStreamSynchronize(stream);
+    if (gexec_) cudaGraphExecDestroy(gexec_);
+    gexec_ = nullptr;
+    for (auto& c : comms)
+      if (c) ncclCommFinalize(c);
+    if (world_comm) ncclCommFinalize(world_comm);
     for (auto& c : comms)
       if (c) ncclCommDestroy(c);
     comms.clear();
@@ -1276,7 +1285,13 @@ void executor_step_async(Executor& e) {
   ++e.steps_since_collect_;
 }
 
-void executor_set_profile(Executor& e, bool on) { e.cfg.profile_gemm = on; }
+void executor_set_profile(Executor& e, bool on) {
+  // NCCL work captured in the step graph must not be followed by eager NCCL
+  // work on the same communicators (observed to hang): profile before capture
+  if (on && e.gexec_ && e.world > 1)
+    throw InvalidArgument("profiling must be enabled before the step graph is captured");
+  e.cfg.profile_gemm = on;
+}
 
 void executor_timer(Executor& e, int stop, float* ms) {
   if (!stop) {
