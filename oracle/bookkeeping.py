@@ -291,6 +291,8 @@ def layout(cluster: dict, model: dict, plan_text: str) -> dict:
     segs = []
     for t in cat:
         cols = t["cols"]
+        # sync group: layer index, -1 embedding, -2 head (final norm + LM head)
+        group = t["layer"] if t["layer"] >= 0 else (-1 if t["kind"] == "embed" else -2)
         hs, cuts = [], set()
         for r in roles:
             for rt in r.tensors:
@@ -302,20 +304,20 @@ def layout(cluster: dict, model: dict, plan_text: str) -> dict:
         for a, b in zip(cuts, cuts[1:]):
             ranks = [(h[0], h[3] + a - h[1]) for h in hs if h[1] <= a and b <= h[2]]
             if len(ranks) >= 2 and b > a:
-                segs.append(([x[0] for x in ranks], [x[1] for x in ranks], b - a))
+                segs.append(([x[0] for x in ranks], [x[1] for x in ranks], b - a, group))
     merged = []
     for sg in segs:
         if merged:
-            mr, ml, mlen = merged[-1]
-            if mr == sg[0] and all(ml[i] + mlen == sg[1][i] for i in range(len(mr))):
-                merged[-1] = (mr, ml, mlen + sg[2])
+            mr, ml, mlen, mg = merged[-1]
+            if mr == sg[0] and mg == sg[3] and all(ml[i] + mlen == sg[1][i] for i in range(len(mr))):
+                merged[-1] = (mr, ml, mlen + sg[2], mg)
                 continue
         merged.append(sg)
     buckets = [[] for _ in range(n)]
-    for ranks, locs, ln in merged:
+    for ranks, locs, ln, grp in merged:
         ci = intern(ranks)
         for rk, lo in zip(ranks, locs):
-            buckets[rk].append({"comm": ci, "offset": lo, "count": ln})
+            buckets[rk].append({"comm": ci, "offset": lo, "count": ln, "group": grp})
 
     out_ranks = []
     for r in roles:

@@ -426,13 +426,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t q_addr = smem_u32(sQ + slot * C::TILE);
         const uint32_t do_addr = smem_u32(sDO + slot * C::TILE);
         mbar_wait(&qdo_full[slot], (t >> 1) & 1);
-        mbar_wait(dq_empty, (t & 1) ^ 1);  // S region (holds dQ_{t-1}) read out
+        mbar_wait(ds_full, (t & 1) ^ 1);  // S region: S_{t-1} fully read (dS_{t-1} done)
         tc_fence_after();
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks)
           tc_mma_f16(tbase + cS, kdesc(k_addr, ks), kdesc(q_addr, ks), id_sp, ks > 0 ? 1u : 0u);
         tc_commit(s_full);
-        mbar_wait(ds_full, (t & 1) ^ 1);  // dP region (dP_{t-1}) consumed
+        mbar_wait(dq_empty, (t & 1) ^ 1);  // dP region: dQ_{t-1} read out
         tc_fence_after();
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks)
@@ -451,9 +451,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int ks = 0; ks < T / 16; ++ks)
           tc_mma_f16(tbase + cK, kdesc(pd_addr, ks), mnview<0>(q_addr, ks), id_acc,
                      (t > 0 || ks > 0) ? 1u : 0u);
+        // dQ_t into the dP region (dP_t consumed by dS_t): S_{t+1} can be issued
+        // at once and overlaps the dQ epilogue of the softmax warps
 #pragma unroll
         for (int ks = 0; ks < T / 16; ++ks)
-          tc_mma_f16(tbase + cS, mnview<0>(pd_addr, ks), mnview<0>(k_addr, ks), id_dq,
+          tc_mma_f16(tbase + cP, mnview<0>(pd_addr, ks), mnview<0>(k_addr, ks), id_dq,
                      ks > 0 ? 1u : 0u);
         tc_commit(dq_full);
         tc_commit(&qdo_empty[slot]);
@@ -466,15 +468,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int kr = ew * 32 + lane;              // key row within the tile (TMEM lane)
     const uint32_t lane_off = uint32_t(ew * 32) << 16;
     uint8_t* stage = sPD + ew * (32 * 64 * 4);  // dQ staging: [32 rows][64 fp32] per warp
+    const long long z0 = ((long long)b * p.nh + h) * p.S + (long long)kt * T;
+    float nlse = p.lse[z0 + tid], ndel = p.delta[z0 + tid];  // prefetched statistics
     for (int t = 0; t < ntiles; ++t) {
       const int i = kt + t;
       const bool diag = t == 0;
       const long long zq = ((long long)b * p.nh + h) * p.S + (long long)i * T;
+      // this warp's dQ reduce of tile t-1 must have read its staging area (the
+      // staging areas overlap other warps' P rows) before anyone writes P_t
+      if (lane == 0) bulk_wait_read<0>();
       // per-query statistics of this tile, shared by the four warps
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      sLse[tid] = p.lse[zq + tid];
-      sDel[tid] = p.delta[zq + tid];
+      sLse[tid] = nlse;
+      sDel[tid] = ndel;
       asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (t + 1 < ntiles) {
+        nlse = p.lse[zq + T + tid];
+        ndel = p.delta[zq + T + tid];
+      }
       // P^T
       mbar_wait(s_full, t & 1);
       tc_fence_after();
@@ -544,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           uint32_t v[32];
-          tmem_ld_32x32b_x32(tbase + lane_off + cS + uint32_t(half * 64 + c * 32), v);
+          tmem_ld_32x32b_x32(tbase + lane_off + cP + uint32_t(half * 64 + c * 32), v);
           tmem_ld_wait();
 #pragma unroll
           for (int q = 0; q < 8; ++q)
@@ -558,7 +569,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_reduce_add_4d(&tmDQ, stage, h * D + half * 64, b * p.S + qrow, 0, 0);
           tma_reduce_add_4d(&tmDQ, stage + 4096, h * D + half * 64 + 32, b * p.S + qrow, 0, 0);
           bulk_commit();
-          bulk_wait_read<0>();
+          if (half + 1 < D / 64) bulk_wait_read<0>();  // staging reused by the next half
         }
         __syncwarp();
       }
@@ -566,6 +577,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(dq_empty);
     }
+    if (lane == 0) bulk_wait_all();
     // dK, dV of this key tile -> bf16 into the dqkv buffer
     mbar_wait(dkv_full, 0);
     tc_fence_after();

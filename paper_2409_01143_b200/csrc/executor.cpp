@@ -72,6 +72,7 @@ ExecConfig parse_exec_config(const std::string& text) {
       else if (k == "profile_gemm") c.profile_gemm = v.get<bool>();
       else if (k == "cuda_graph") c.cuda_graph = v.get<bool>();
       else if (k == "attention") c.attention = v.get<std::string>();
+      else if (k == "dp_overlap") c.dp_overlap = v.get<bool>();
       else throw ParseError("exec config: unknown key '" + k + "'");
     } catch (const nlohmann::json::exception& e) {
       throw ParseError("exec config: bad value for '" + k + "'");
@@ -214,6 +215,7 @@ class Executor {
     // work) before the communicators: destroying a communicator still
     // referenced by a graph exec blocks
     if (stream) cudaStreamSynchronize(stream);
+    if (cstream) cudaStreamSynchronize(cstream);
     if (gexec_) cudaGraphExecDestroy(gexec_);
     gexec_ = nullptr;
     for (auto& c : comms)
@@ -246,6 +248,13 @@ class Executor {
     mark_pool_.clear();
     if (gexec_) cudaGraphExecDestroy(gexec_);
     gexec_ = nullptr;
+    for (auto& g : groups_)
+      if (g.ready) cudaEventDestroy(g.ready);
+    groups_.clear();
+    if (join_ev_) cudaEventDestroy(join_ev_);
+    join_ev_ = nullptr;
+    if (own_cstream && cstream) cudaStreamDestroy(cstream);
+    cstream = nullptr;
     if (own_stream && stream) cudaStreamDestroy(stream);
     stream = nullptr;
   }
@@ -297,6 +306,8 @@ class Executor {
     if (role.active) {
       allocate();
       init_params();
+      build_groups();
+      if (!cstream) cfg.dp_overlap = false;
     } else {
       HX_CUDA(cudaMalloc(&idle_loss_, 256));
       loss_acc = idle_loss_;
@@ -320,6 +331,8 @@ class Executor {
     }
     HX_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     own_stream = true;
+    HX_CUDA(cudaStreamCreateWithFlags(&cstream, cudaStreamNonBlocking));
+    own_cstream = true;
     if ((cfg.sm_cap == "cta" || cfg.sm_cap == "green") && want < sm_total) {
       gemm_set_sm_limit(want);
       sm_applied = want;
@@ -363,6 +376,11 @@ class Executor {
     if (pStream(&s, green, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) return false;
     stream = reinterpret_cast<cudaStream_t>(s);
     own_stream = true;
+    CUstream s2;  // comm stream inside the same SM partition
+    if (pStream(&s2, green, CU_STREAM_NON_BLOCKING, 0) == CUDA_SUCCESS) {
+      cstream = reinterpret_cast<cudaStream_t>(s2);
+      own_cstream = true;
+    }
     sm_applied = int(part.sm.smCount);
     gemm_set_sm_limit(sm_applied);
     return true;
@@ -945,6 +963,7 @@ class Executor {
       k_rmsnorm_bwd(dy16, nullptr, sl.x[size_t(nl)], sl.rstdf, final_norm.p32, nullptr, cur, curb,
                     final_norm.g32, int(M), int(H), coef_, stream);
       kcheck("rmsnorm_bwd");
+      group_ready(kGroupHead);
     } else {
       HX_CUDA(cudaMemcpyAsync(cur, dx_top, size_t(M * H) * 4, cudaMemcpyDeviceToDevice, stream));
       k_cast_bf16(cur, curb, M * H, stream);
@@ -954,10 +973,12 @@ class Executor {
       // dxi aliases the ping-pong partner; dxb reused in place (row-local ops)
       layer_bwd(sl, l, cur, curb, nxt, curb);
       std::swap(cur, nxt);
+      group_ready(int(role.layer_start + l));
     }
     if (role.first_stage) {
       k_embed_bwd(tok_of(mbi), cur, embed.g32, int(M), int(S), int(H), stream);
       kcheck("embed_bwd");
+      group_ready(kGroupEmbed);
     }
     bwd_out_ = cur;
   }
@@ -1006,6 +1027,7 @@ class Executor {
     int64_t next_bwd = 0;
     auto do_bwd = [&](int64_t mbi) {
       accum_first_ = next_bwd == 0;
+      last_mb_ = next_bwd == n - 1;
       backward(mbi, slot_of(mbi), grecv);
       ++next_bwd;
     };
@@ -1044,6 +1066,95 @@ class Executor {
       do_bwd(i);
       send_bwd(bwd_out_);
       if (pp) mark("nccl_pp");
+    }
+  }
+
+  // ------------------------------------------------------------ DP overlap
+  // Gradients become final group by group during the backward of the last
+  // micro-batch (head, layers descending, embedding).  Each group's DP work --
+  // sample-weighted scale + bf16 cast, chunk-matched allreduce, AdamW -- runs
+  // on a second stream as soon as the group is final, overlapping the backward
+  // of the remaining layers.  Every rank walks the groups in the same global
+  // order, so per-communicator call order matches across ranks.
+  struct SyncGroup {
+    int id = 0;
+    std::vector<size_t> tensors;   // indices into role.tensors
+    std::vector<DpBucket> buckets;
+    cudaEvent_t ready = nullptr;
+  };
+  std::vector<SyncGroup> groups_;
+  cudaStream_t cstream = nullptr;
+  bool own_cstream = false;
+  cudaEvent_t join_ev_ = nullptr;
+  bool last_mb_ = false;
+
+  void build_groups() {
+    std::map<int, size_t> idx;
+    for (size_t i = 0; i < role.tensors.size(); ++i) {
+      const int g = sync_group(L.tensors[size_t(role.tensors[i].spec)]);
+      if (!idx.count(g)) {
+        idx[g] = groups_.size();
+        SyncGroup sg;
+        sg.id = g;
+        HX_CUDA(cudaEventCreateWithFlags(&sg.ready, cudaEventDisableTiming));
+        groups_.push_back(sg);
+      }
+      groups_[idx[g]].tensors.push_back(i);
+    }
+    for (const auto& b : L.dp_buckets[size_t(rank)]) groups_[idx.at(b.group)].buckets.push_back(b);
+    HX_CUDA(cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming));
+  }
+
+  // enqueue the DP work of one group on stream `s`
+  void group_work(const SyncGroup& g, cudaStream_t s) {
+    const bool bf = G16 != nullptr;
+    for (size_t ti : g.tensors) {
+      const RankTensor& rt = role.tensors[ti];
+      const int64_t cnt = rt.rows * L.tensors[size_t(rt.spec)].cols;
+      if (!covered(rt.offset, cnt)) continue;
+      const float sc = float(role.dp_weight / double(rt.multiplicity));
+      if (bf)
+        k_scale_cast(G32 + rt.offset, G16 + rt.offset, cnt, sc, s);
+      else
+        k_scale(G32 + rt.offset, cnt, sc, s);
+      kcheck("scale");
+    }
+    if (!g.buckets.empty()) {
+      HX_NCCL(ncclGroupStart());
+      for (const auto& b : g.buckets) {
+        if (bf)
+          HX_NCCL(ncclAllReduce(G16 + b.offset, G16 + b.offset, size_t(b.count), ncclBfloat16,
+                                ncclSum, comms[size_t(b.comm)], s));
+        else
+          HX_NCCL(ncclAllReduce(G32 + b.offset, G32 + b.offset, size_t(b.count), ncclFloat32,
+                                ncclSum, comms[size_t(b.comm)], s));
+        ++nccl_calls_step;
+      }
+      HX_NCCL(ncclGroupEnd());
+    }
+    for (size_t ti : g.tensors) {
+      const RankTensor& rt = role.tensors[ti];
+      const TensorSpec& ts = L.tensors[size_t(rt.spec)];
+      const int64_t cnt = rt.rows * ts.cols;
+      const float wd = ts.decay ? cfg.weight_decay : 0.f;
+      const bool cov = covered(rt.offset, cnt);
+      const bf16* g16 = cov && bf ? G16 + rt.offset : nullptr;
+      const float* g32 = g16 ? nullptr : G32 + rt.offset;
+      const float gscale = cov ? 1.f : float(role.dp_weight / double(rt.multiplicity));
+      k_adamw(P32 + rt.offset, P16 + rt.offset, Mo + rt.offset, Vo + rt.offset, g16, g32, cnt,
+              gscale, cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, wd, 0.f, 0.f, s, sp_);
+      kcheck("adamw");
+    }
+  }
+
+  // group `id` is final on the compute stream: hand it to the comm stream
+  void group_ready(int id) {
+    if (!cfg.dp_overlap || !last_mb_) return;
+    for (auto& g : groups_) {
+      if (g.id != id) continue;
+      HX_CUDA(cudaEventRecord(g.ready, stream));
+      HX_CUDA(cudaStreamWaitEvent(cstream, g.ready, 0));
+      group_work(g, cstream);
     }
   }
 
@@ -1179,8 +1290,21 @@ class Executor {
     }
     mark("prologue");
     cudaEventRecord(ev[1], stream);
+    if (cfg.dp_overlap) {
+      // fork the comm stream into this step (and into the graph when capturing)
+      HX_CUDA(cudaEventRecord(join_ev_, stream));
+      HX_CUDA(cudaStreamWaitEvent(cstream, join_ev_, 0));
+    }
     run_pipeline();
-    dp_sync_and_update();
+    if (cfg.dp_overlap) {
+      HX_CUDA(cudaEventRecord(join_ev_, cstream));
+      HX_CUDA(cudaStreamWaitEvent(stream, join_ev_, 0));
+      cudaEventRecord(ev[2], stream);
+      cudaEventRecord(ev[3], stream);
+      cudaEventRecord(ev[4], stream);
+    } else {
+      dp_sync_and_update();
+    }
     finish_loss();
     cudaEventRecord(ev[5], stream);
   }

@@ -20,6 +20,7 @@ struct ExecConfig {
   bool profile_gemm = false;          // per-GEMM CUDA events (roofline evidence); eager
   bool cuda_graph = true;             // replay the captured step graph (after step 0)
   std::string attention = "fused";    // "fused" (flash, tcgen05) | "unfused" (GEMM+softmax)
+  bool dp_overlap = true;             // DP sync + AdamW per layer on a second stream
 };
 
 ExecConfig parse_exec_config(const std::string& text);

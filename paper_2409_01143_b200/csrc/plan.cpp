@@ -382,6 +382,15 @@ void rows_of(const TensorSpec& s, const RankRole& r, const Model& m, int64_t* ro
   }
 }
 
+}  // namespace
+
+int sync_group(const TensorSpec& t) {
+  if (t.layer >= 0) return t.layer;
+  return t.id == kEmbed ? kGroupEmbed : kGroupHead;
+}
+
+namespace {
+
 int intern_set(std::vector<std::vector<int>>& sets, std::map<std::vector<int>, int>& idx,
                std::vector<int> s) {
   std::sort(s.begin(), s.end());
@@ -531,10 +540,11 @@ Layout build_layout(const std::string& cluster_json, const std::string& model_js
   }
   // holders per tensor
   struct Holder { int rank; int64_t b, e, local; };
-  struct Seg { std::vector<int> ranks; std::vector<int64_t> local; int64_t len; };
+  struct Seg { std::vector<int> ranks; std::vector<int64_t> local; int64_t len; int group; };
   std::vector<Seg> segs;
   for (int s = 0; s < int(L.tensors.size()); ++s) {
     const int64_t cols = L.tensors[size_t(s)].cols;
+    const int group = sync_group(L.tensors[size_t(s)]);
     std::vector<Holder> hs;
     std::vector<int64_t> cuts;
     for (int r = 0; r < n; ++r)
@@ -549,6 +559,7 @@ Layout build_layout(const std::string& cluster_json, const std::string& model_js
     for (size_t k = 0; k + 1 < cuts.size(); ++k) {
       Seg sg;
       sg.len = cuts[k + 1] - cuts[k];
+      sg.group = group;
       for (const auto& h : hs)
         if (h.b <= cuts[k] && cuts[k + 1] <= h.e) {
           sg.ranks.push_back(h.rank);
@@ -562,7 +573,10 @@ Layout build_layout(const std::string& cluster_json, const std::string& model_js
   for (auto& sg : segs) {
     if (!merged.empty()) {
       Seg& b = merged.back();
-      bool ok = b.ranks == sg.ranks;
+      // buckets never span two sync groups (layer / embedding / head), so each
+      // becomes reducible as soon as its group's backward of the last
+      // micro-batch is done
+      bool ok = b.ranks == sg.ranks && b.group == sg.group;
       for (size_t i = 0; ok && i < sg.ranks.size(); ++i) ok = b.local[i] + b.len == sg.local[i];
       if (ok) {
         b.len += sg.len;
@@ -574,7 +588,7 @@ Layout build_layout(const std::string& cluster_json, const std::string& model_js
   for (const auto& sg : merged) {
     int ci = intern_set(L.comm_sets, set_idx, sg.ranks);
     for (size_t i = 0; i < sg.ranks.size(); ++i)
-      L.dp_buckets[size_t(sg.ranks[i])].push_back({ci, sg.local[i], sg.len});
+      L.dp_buckets[size_t(sg.ranks[i])].push_back({ci, sg.local[i], sg.len, sg.group});
   }
   return L;
 }
@@ -629,7 +643,8 @@ std::string layout_json(const Layout& L) {
       jr["tensors"] = ts;
       ojson bk = ojson::array();
       for (const auto& b : L.dp_buckets[size_t(r)])
-        bk.push_back({{"comm", b.comm}, {"offset", b.offset}, {"count", b.count}});
+        bk.push_back({{"comm", b.comm}, {"offset", b.offset}, {"count", b.count},
+                      {"group", b.group}});
       jr["dp_buckets"] = bk;
     }
     j["ranks"].push_back(std::move(jr));

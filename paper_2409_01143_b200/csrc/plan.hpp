@@ -122,7 +122,13 @@ struct RankRole {
 struct DpBucket {
   int comm = -1;          // index into Layout::comm_sets
   int64_t offset = 0, count = 0;
+  int group = 0;          // sync group (layer index, kGroupEmbed, kGroupHead)
 };
+
+// gradients become final in backward order: head, layers descending, embedding
+constexpr int kGroupEmbed = -1;
+constexpr int kGroupHead = -2;
+int sync_group(const TensorSpec& t);
 
 struct ScaleSeg {
   int64_t offset = 0, count = 0;
