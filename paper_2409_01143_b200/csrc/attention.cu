@@ -297,6 +297,275 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------------------------------------------ forward, 2 Q tiles
+// CTA = one (sample, head) and the query-tile pair (2t, 2t+1).  Two softmax
+// warpgroups (A: warps 4-7, B: warps 8-11) ping-pong: while one computes its
+// softmax the tensor core runs the other tile's S or PV product.  K/V tiles
+// are loaded once for both query tiles (K double-buffered, V single).
+// TMEM: S_A | S_B | O_A | O_B (4 x 128 columns).  Register budget via
+// setmaxnreg: the producer/MMA warpgroup drops to 56, softmax warpgroups get 224.
+constexpr int kThreads2 = 384;
+
+template <int D>
+struct Fwd2Cfg {
+  static constexpr uint32_t TILE = T * D * 2;
+  static constexpr uint32_t P_BYTES = T * T * 2;
+  static constexpr uint32_t SMEM = 1024 + 2 * TILE /*Q*/ + 2 * TILE /*K*/ + TILE /*V*/ +
+                                   2 * P_BYTES + 256;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads2, 1)
+    attn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
+  using C = Fwd2Cfg<D>;
+  constexpr int DA = D / 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                  // [2 tiles]
+  uint8_t* sK = sQ + 2 * C::TILE;      // [2 slots]
+  uint8_t* sV = sK + 2 * C::TILE;      // [1 slot]
+  uint8_t* sP = sV + C::TILE;          // [2 tiles]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + 2 * C::P_BYTES);
+  uint64_t* q_full = bar;        // Q_A + Q_B
+  uint64_t* k_full = bar + 1;    // [2]
+  uint64_t* k_empty = bar + 3;   // [2]
+  uint64_t* v_full = bar + 5;
+  uint64_t* v_empty = bar + 6;
+  uint64_t* s_full = bar + 7;    // [2 tiles]
+  uint64_t* s_empty = bar + 9;   // [2 tiles]
+  uint64_t* p_full = bar + 11;   // [2 tiles]
+  uint64_t* o_full = bar + 13;   // [2 tiles]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 15);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int nqt = p.S / T;
+  const int npairs = (nqt + 1) / 2;
+  const int pr = npairs - 1 - int(blockIdx.x % npairs);  // heaviest pairs first
+  const int zh = int(blockIdx.x / npairs);
+  const int h = zh % p.nh;
+  const int b = zh / p.nh;
+  const int qa = 2 * pr;                 // query tile of warpgroup A
+  const bool has_b = qa + 1 < nqt;       // query tile qa+1 of warpgroup B
+  const int nt_a = qa + 1;               // key tiles visited by A / B
+  const int nt_b = has_b ? qa + 2 : 0;
+  const int nkv = has_b ? nt_b : nt_a;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&o_full[i], 1);
+    }
+    mbar_init(v_full, 1);
+    mbar_init(v_empty, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+    if (warp == 0 && lane == 0) {
+      mbar_arrive_expect_tx(q_full, (has_b ? 2 : 1) * C::TILE);
+      for (int a = 0; a < DA; ++a) {
+        tma_load_4d(sQ + a * ATOM, &tmQ, q_full, a * 64, qa * T, h, b);
+        if (has_b) tma_load_4d(sQ + C::TILE + a * ATOM, &tmQ, q_full, a * 64, (qa + 1) * T, h, b);
+      }
+      for (int j = 0; j < nkv; ++j) {
+        const int slot = j & 1;
+        mbar_wait(&k_empty[slot], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&k_full[slot], C::TILE);
+        for (int a = 0; a < DA; ++a)
+          tma_load_4d(sK + slot * C::TILE + a * ATOM, &tmK, &k_full[slot], a * 64, j * T, h, b);
+        mbar_wait(v_empty, (j & 1) ^ 1);
+        mbar_arrive_expect_tx(v_full, C::TILE);
+        for (int kb = 0; kb < 2; ++kb)
+          for (int a = 0; a < DA; ++a)
+            tma_load_4d(sV + kb * (DA * 8192) + a * 8192, &tmV, v_full, a * 64, j * T + kb * 64, h, b);
+      }
+    } else if (warp == 1 && lane == 0) {
+      const uint32_t id_s = idesc_bf16(T, T, 0, 0);
+      const uint32_t id_o = idesc_bf16(T, D, 0, 1);
+      mbar_wait(q_full, 0);
+      auto issue_s = [&](int g, int j) {  // S_g(j) = Q_g K_j^T
+        const int slot = j & 1;
+        mbar_wait(&k_full[slot], (j >> 1) & 1);
+        mbar_wait(&s_empty[g], (j & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t q_addr = smem_u32(sQ + g * C::TILE);
+        const uint32_t k_addr = smem_u32(sK + slot * C::TILE);
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks)
+          tc_mma_f16(tbase + uint32_t(g * T), kdesc(q_addr, ks), kdesc(k_addr, ks), id_s,
+                     ks > 0 ? 1u : 0u);
+        tc_commit(&s_full[g]);
+      };
+      auto issue_o = [&](int g, int j) {  // O_g += P_g(j) V_j
+        mbar_wait(&p_full[g], j & 1);
+        tc_fence_after();
+        const uint32_t p_addr = smem_u32(sP + g * C::P_BYTES);
+        const uint32_t v_addr = smem_u32(sV);
+#pragma unroll
+        for (int ks = 0; ks < T / 16; ++ks)
+          tc_mma_f16(tbase + uint32_t(2 * T + g * T), kdesc(p_addr, ks), mndesc<DA>(v_addr, ks),
+                     id_o, (j > 0 || ks > 0) ? 1u : 0u);
+        tc_commit(&o_full[g]);
+      };
+      if (nt_a > 0) issue_s(0, 0);
+      if (has_b) issue_s(1, 0);
+      for (int j = 0; j < nkv; ++j) {
+        const bool a_on = j < nt_a, b_on = j < nt_b;
+        mbar_wait(v_full, j & 1);
+        if (a_on) {
+          issue_o(0, j);
+          if (j + 1 < nt_a) issue_s(0, j + 1);
+        }
+        if (b_on) {
+          issue_o(1, j);
+          if (j + 1 < nt_b) issue_s(1, j + 1);
+        }
+        tc_commit(v_empty);               // V_j consumed once both PV products finish
+        tc_commit(&k_empty[j & 1]);       // K_j consumed by both S products
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
+    const int g = (warp - 4) / 4;  // 0 = A, 1 = B
+    const int ew = (warp - 4) % 4;
+    const int qt = qa + g;
+    const int ntiles = g == 0 ? nt_a : nt_b;
+    if (ntiles > 0) {
+      const int r = ew * 32 + lane;
+      const uint32_t lane_off = uint32_t(ew * 32) << 16;
+      const uint32_t s_col = uint32_t(g * T), o_col = uint32_t(2 * T + g * T);
+      uint8_t* myP = sP + g * C::P_BYTES;
+      constexpr float kSlack = 8.f;
+      float m = -FLT_MAX, l = 0.f;
+      for (int j = 0; j < ntiles; ++j) {
+        const bool diag = j == qt;
+        mbar_wait(&s_full[g], j & 1);
+        tc_fence_after();
+        uint32_t sv[T];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t* v = sv + c * 32;
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+              "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+                "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]),
+                "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+                "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+                "=r"(v[30]), "=r"(v[31])
+              : "r"(tbase + lane_off + s_col + uint32_t(c * 32)));
+        }
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[g]);
+        float mx[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mx[k] = -FLT_MAX;
+#pragma unroll
+        for (int i = 0; i < T; ++i)
+          if (!diag || i <= r) mx[i % 8] = fmaxf(mx[i % 8], __uint_as_float(sv[i]));
+        float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                         fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        mt *= p.scale_log2;
+        if (j > 0) {  // PV_{j-1} done: P buffer free and O stable
+          mbar_wait(&o_full[g], (j - 1) & 1);
+          tc_fence_after();
+        }
+        if (__any_sync(0xffffffffu, mt > m + kSlack)) {
+          const float m_new = fmaxf(m, mt);
+          const float alpha = ex2(m - m_new);
+          if (j > 0) {
+#pragma unroll 1
+            for (int c = 0; c < D / 32; ++c) {
+              uint32_t v[32];
+              tmem_ld_32x32b_x32(tbase + lane_off + o_col + uint32_t(c * 32), v);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+              tmem_st_32x32b_x32(tbase + lane_off + o_col + uint32_t(c * 32), v);
+            }
+            tmem_st_wait();
+          }
+          l *= alpha;
+          m = m_new;
+        }
+        float lsp[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) lsp[k] = 0.f;
+#pragma unroll
+        for (int q = 0; q < T / 8; ++q) {
+          float pv[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int i = q * 8 + k;
+            const float e = ex2(fmaf(__uint_as_float(sv[i]), p.scale_log2, -m));
+            pv[k] = (!diag || i <= r) ? e : 0.f;
+            lsp[k] += pv[k];
+          }
+          uint4 w;
+          w.x = pack_bf16x2(pv[0], pv[1]);
+          w.y = pack_bf16x2(pv[2], pv[3]);
+          w.z = pack_bf16x2(pv[4], pv[5]);
+          w.w = pack_bf16x2(pv[6], pv[7]);
+          *reinterpret_cast<uint4*>(myP + kchunk(r, q)) = w;
+        }
+        l += ((lsp[0] + lsp[1]) + (lsp[2] + lsp[3])) + ((lsp[4] + lsp[5]) + (lsp[6] + lsp[7]));
+        tc_fence_before();
+        fence_async_shared();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[g]);
+      }
+      mbar_wait(&o_full[g], (ntiles - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / l;
+      const int qi = qt * T + r;
+      __nv_bfloat16* dst = p.out + ((long long)b * p.S + qi) * p.ldo + (long long)h * D;
+#pragma unroll 1
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tbase + lane_off + o_col + uint32_t(c * 32), v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 w;
+          w.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]) * inv, __uint_as_float(v[8 * q + 1]) * inv);
+          w.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv);
+          w.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv);
+          w.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv);
+          reinterpret_cast<uint4*>(dst)[c * 4 + q] = w;
+        }
+      }
+      p.lse[((long long)b * p.nh + h) * p.S + qi] = m + log2f(l);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
 // ------------------------------------------------------------------ backward
 // CTA = one (sample, head, 128-key tile kt); loops over query tiles i >= kt.
 // Transposed formulation so TMEM rows are keys:
@@ -666,6 +935,7 @@ __global__ void attn_dq_cast_kernel(const float* __restrict__ dq, __nv_bfloat16*
 }
 
 // ------------------------------------------------------------------ host
+int g_fwd_variant = 2;  // 2 = two query tiles per CTA (ping-pong), 1 = one tile
 PFN_cuTensorMapEncodeTiled_v12000 g_enc = nullptr;
 std::once_flag g_enc_once;
 
@@ -706,10 +976,14 @@ bool encode_f32(CUtensorMap* map, float* base, long long cols, long long rows) {
 template <int D>
 cudaError_t launch_fwd(const AttnDesc& a, cudaStream_t s) {
   using C = FwdCfg<D>;
+  using C2 = Fwd2Cfg<D>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<D>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(attn_fwd2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(C2::SMEM));
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -727,8 +1001,13 @@ cudaError_t launch_fwd(const AttnDesc& a, cudaStream_t s) {
   p.mb = a.mb;
   p.ldo = a.nh * D;
   p.scale_log2 = a.scale * 1.4426950408889634f;
-  const int grid = (a.S / T) * a.nh * a.mb;
-  attn_fwd_kernel<D><<<grid, kThreads, C::SMEM, s>>>(q, k, v, p);
+  if (g_fwd_variant == 2) {
+    const int grid = ((a.S / T + 1) / 2) * a.nh * a.mb;
+    attn_fwd2_kernel<D><<<grid, kThreads2, C2::SMEM, s>>>(q, k, v, p);
+  } else {
+    const int grid = (a.S / T) * a.nh * a.mb;
+    attn_fwd_kernel<D><<<grid, kThreads, C::SMEM, s>>>(q, k, v, p);
+  }
   return cudaGetLastError();
 }
 
@@ -776,6 +1055,8 @@ cudaError_t launch_bwd(const AttnBwdDesc& a, cudaStream_t s) {
 }
 
 }  // namespace
+
+void attention_fwd_variant(int v) { g_fwd_variant = v == 1 ? 1 : 2; }
 
 cudaError_t attention_fwd(const AttnDesc& a, cudaStream_t s) {
   if (a.S % T != 0 || a.S <= 0) return cudaErrorInvalidValue;

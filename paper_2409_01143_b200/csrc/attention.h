@@ -19,6 +19,8 @@ struct AttnDesc {
 
 // forward: out = softmax(scale * q k^T, causal) v ; lse saved for the backward
 cudaError_t attention_fwd(const AttnDesc& a, cudaStream_t s);
+// 2 (default): two query tiles per CTA with ping-pong softmax warpgroups; 1: one tile
+void attention_fwd_variant(int v);
 
 struct AttnBwdDesc {
   const __nv_bfloat16* qkv = nullptr;
