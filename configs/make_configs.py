@@ -124,7 +124,7 @@ PLANNED = {
                           "state_multiplier": 2.5}),
     # N=4 scaling point
     "llama7b_4l_4_asym": ("b200_4_tiers", "llama7b_4l", "schedule",
-                          {"global_batch": 16, "iterations": 30, "seed": 0, "threads": 8,
+                          {"global_batch": 48, "iterations": 30, "seed": 0, "threads": 8,
                            "state_multiplier": 2.5}),
     "llama7b_4l_2_asym": ("b200_2_capped", "llama7b_4l", "schedule",
                           {"global_batch": 8, "iterations": 20, "seed": 0, "threads": 8,
@@ -134,7 +134,7 @@ PLANNED = {
                           {"global_batch": 8, "iterations": 20, "seed": 0, "threads": 8,
                            "state_multiplier": 2.5}),
     "llama7b_4l_4_even": ("b200_4_eq", "llama7b_4l", "symmetric",
-                          {"global_batch": 16, "iterations": 30, "seed": 0, "threads": 8,
+                          {"global_batch": 48, "iterations": 30, "seed": 0, "threads": 8,
                            "state_multiplier": 2.5}),
     "llama7b_8_eq_even": ("b200_8_eq", "llama7b", "symmetric",
                           {"global_batch": 64, "iterations": 50, "seed": 0, "threads": 8,
