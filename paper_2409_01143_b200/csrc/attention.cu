@@ -625,7 +625,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* dq_full = bar + 10;
   uint64_t* dq_empty = bar + 11;
   uint64_t* dkv_full = bar + 12;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 13);
+  uint64_t* s_read = bar + 13;     // softmax warps hold S_t in registers
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 14);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -657,6 +658,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(dq_full, 1);
     mbar_init(dq_empty, 4);
     mbar_init(dkv_full, 1);
+    mbar_init(s_read, 4);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(tslot);
@@ -690,17 +692,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t id_dq = idesc_bf16(T, D, 1, 1);   // A MN-major (dS view), B MN-major (K view)
       const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), pd_addr = smem_u32(sPD);
       mbar_wait(kv_full, 0);
+      mbar_wait(&qdo_full[0], 0);
+      tc_fence_after();
+#pragma unroll
+      for (int ks = 0; ks < D / 16; ++ks)
+        tc_mma_f16(tbase + cS, kdesc(k_addr, ks), kdesc(smem_u32(sQ), ks), id_sp, ks > 0 ? 1u : 0u);
+      tc_commit(s_full);
       for (int t = 0; t < ntiles; ++t) {
         const int slot = t & 1;
         const uint32_t q_addr = smem_u32(sQ + slot * C::TILE);
         const uint32_t do_addr = smem_u32(sDO + slot * C::TILE);
-        mbar_wait(&qdo_full[slot], (t >> 1) & 1);
-        mbar_wait(ds_full, (t & 1) ^ 1);  // S region: S_{t-1} fully read (dS_{t-1} done)
-        tc_fence_after();
-#pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks)
-          tc_mma_f16(tbase + cS, kdesc(k_addr, ks), kdesc(q_addr, ks), id_sp, ks > 0 ? 1u : 0u);
-        tc_commit(s_full);
         mbar_wait(dq_empty, (t & 1) ^ 1);  // dP region: dQ_{t-1} read out
         tc_fence_after();
 #pragma unroll
@@ -714,6 +715,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_mma_f16(tbase + cV, kdesc(pd_addr, ks), mnview<0>(do_addr, ks), id_acc,
                      (t > 0 || ks > 0) ? 1u : 0u);
         tc_commit(pds_free);
+        if (t + 1 < ntiles) {
+          // S_{t+1} as soon as the softmax warps hold S_t in registers: it runs
+          // while they compute dS_t
+          const int ns = (t + 1) & 1;
+          mbar_wait(&qdo_full[ns], ((t + 1) >> 1) & 1);
+          mbar_wait(s_read, t & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int ks = 0; ks < D / 16; ++ks)
+            tc_mma_f16(tbase + cS, kdesc(k_addr, ks), kdesc(smem_u32(sQ + ns * C::TILE), ks), id_sp,
+                       ks > 0 ? 1u : 0u);
+          tc_commit(s_full);
+        }
         mbar_wait(ds_full, t & 1);
         tc_fence_after();
 #pragma unroll
@@ -755,30 +769,40 @@ __global__ void __launch_bounds__(kThreads, 1)
         nlse = p.lse[zq + T + tid];
         ndel = p.delta[zq + T + tid];
       }
-      // P^T
+      // P^T, kept in registers for the dS pass
       mbar_wait(s_full, t & 1);
       tc_fence_after();
+      uint32_t pu[T];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tbase + lane_off + cS + uint32_t(c * 32), v);
-        tmem_ld_wait();
+      for (int c = 0; c < 4; ++c)
+        tmem_ld_32x32b_x32(tbase + lane_off + cS + uint32_t(c * 32),
+                           *reinterpret_cast<uint32_t(*)[32]>(pu + c * 32));
+      tmem_ld_wait();
+      float pk[T];
 #pragma unroll
-        for (int q8 = 0; q8 < 4; ++q8) {
-          float pr[8];
+      for (int k = 0; k < T; ++k) pk[k] = __uint_as_float(pu[k]);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_read);  // S region may take S_{t+1} now
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int qc = c * 32 + q8 * 8 + k;
-            const float e = ex2(__uint_as_float(v[q8 * 8 + k]) * p.scale_log2 - sLse[qc]);
-            pr[k] = (diag && kr > qc) ? 0.f : e;
-          }
-          uint4 w;
-          w.x = pack_bf16x2(pr[0], pr[1]);
-          w.y = pack_bf16x2(pr[2], pr[3]);
-          w.z = pack_bf16x2(pr[4], pr[5]);
-          w.w = pack_bf16x2(pr[6], pr[7]);
-          *reinterpret_cast<uint4*>(sPD + kchunk(kr, c * 4 + q8)) = w;
+      for (int q8 = 0; q8 < T / 8; ++q8) {
+        const float4 la = *reinterpret_cast<const float4*>(sLse + q8 * 8);
+        const float4 lb = *reinterpret_cast<const float4*>(sLse + q8 * 8 + 4);
+        const float ls[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
+        float pr[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int qc = q8 * 8 + k;
+          const float e = ex2(fmaf(pk[qc], p.scale_log2, -ls[k]));
+          pr[k] = (diag && kr > qc) ? 0.f : e;
+          pk[qc] = pr[k];
         }
+        uint4 w;
+        w.x = pack_bf16x2(pr[0], pr[1]);
+        w.y = pack_bf16x2(pr[2], pr[3]);
+        w.z = pack_bf16x2(pr[4], pr[5]);
+        w.w = pack_bf16x2(pr[6], pr[7]);
+        *reinterpret_cast<uint4*>(sPD + kchunk(kr, q8)) = w;
       }
       fence_async_shared();
       __syncwarp();
@@ -789,19 +813,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        uint32_t sv[32], dv[32];
-        tmem_ld_32x32b_x32(tbase + lane_off + cS + uint32_t(c * 32), sv);
+        uint32_t dv[32];
         tmem_ld_32x32b_x32(tbase + lane_off + cP + uint32_t(c * 32), dv);
         tmem_ld_wait();
 #pragma unroll
         for (int q8 = 0; q8 < 4; ++q8) {
           float ds[8];
+          const float4 da = *reinterpret_cast<const float4*>(sDel + c * 32 + q8 * 8);
+          const float4 db = *reinterpret_cast<const float4*>(sDel + c * 32 + q8 * 8 + 4);
+          const float dl[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             const int qc = c * 32 + q8 * 8 + k;
-            const float pe = ex2(__uint_as_float(sv[q8 * 8 + k]) * p.scale_log2 - sLse[qc]);
-            const float pv = (diag && kr > qc) ? 0.f : pe;
-            ds[k] = pv * (__uint_as_float(dv[q8 * 8 + k]) - sDel[qc]) * p.scale;
+            ds[k] = pk[qc] * (__uint_as_float(dv[q8 * 8 + k]) - dl[k]) * p.scale;
           }
           uint4 w;
           w.x = pack_bf16x2(ds[0], ds[1]);
