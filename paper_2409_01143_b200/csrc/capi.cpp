@@ -323,14 +323,9 @@ hexexec_status hexexec_k_rmsnorm_bwd(const void* dyb, const float* dyf, const fl
                                      const float* rstd, const float* g, const float* dres,
                                      float* dx, void* dxb, float* dg, int M, int H,
                                      void* stream) {
-  float* coef = nullptr;
-  cudaStream_t s = as_stream(stream);
-  if (cudaMallocAsync(&coef, size_t(M) * sizeof(float), s) != cudaSuccess) return HEXEXEC_ERR_CUDA;
   hexexec::k_rmsnorm_bwd(static_cast<const hexexec::bf16*>(dyb), dyf, x, rstd, g, dres, dx,
-                         static_cast<hexexec::bf16*>(dxb), dg, M, H, coef, s);
-  cudaError_t e = cudaGetLastError();
-  cudaFreeAsync(coef, s);
-  return cuda_status(e);
+                         static_cast<hexexec::bf16*>(dxb), dg, M, H, as_stream(stream));
+  return cuda_status(cudaGetLastError());
 }
 
 hexexec_status hexexec_k_rope(void* qkv, int M, int S, int nh, int d, float theta, int inverse,

@@ -192,7 +192,6 @@ class Executor {
        *dqkv = nullptr, *dy16 = nullptr;
   float *dx[2] = {nullptr, nullptr}, *ce_scr = nullptr, *loss_acc = nullptr, *loss_host = nullptr;
   bf16* dxb = nullptr;
-  float* coef_ = nullptr;
   float *delta_ = nullptr, *dq_acc_ = nullptr;
   int32_t* tokens = nullptr;
   int32_t* tokens_pinned = nullptr;
@@ -445,7 +444,6 @@ class Executor {
     arena.reserve(M * H * 2);   // ypart
     arena.reserve(M * F * 2 + M * 2 * F * 2 + M * kr * 2 + M * qkvw * 2);
     arena.reserve(M * H * 4 * 2 + M * H * 2 + M * H * 2);  // dx ping-pong, dxb, dy16
-    arena.reserve(M * 4);                                  // rmsnorm bwd row coefficients
     if (role.last_stage) arena.reserve(M * Vr * 4 + 5 * M * 4);
     arena.reserve(256);                                    // loss
     arena.reserve(role.batch * (S + 1) * 4);               // tokens
@@ -496,7 +494,6 @@ class Executor {
     dx[1] = arena.take<float>(M * H);
     dxb = arena.take<bf16>(M * H);
     dy16 = arena.take<bf16>(M * H);
-    coef_ = arena.take<float>(M);
     if (role.last_stage) {
       logits = arena.take<float>(M * Vr);
       ce_scr = arena.take<float>(5 * M);
@@ -848,7 +845,7 @@ class Executor {
     float* dxm = dxi;
     bf16* dxmb = dxib;
     k_rmsnorm_bwd(dy16, nullptr, a.x_mid, a.rstd2, w.mlp_norm.p32, dxo, dxm, dxmb, w.mlp_norm.g32,
-                  int(M), int(H), coef_, stream);
+                  int(M), int(H), stream);
     kcheck("rmsnorm_bwd");
     // attention: O projection
     gemm(g2(M, kr, H, dxmb, 0, H, w.wo.p16, 0, H, dattn, kr, 0));
@@ -869,7 +866,7 @@ class Executor {
     tp_allreduce_bf16(dy16, M * H);
     // dx_in = dx_mid + rmsnorm_bwd(dxn): in place over dx_mid (row-local)
     k_rmsnorm_bwd(dy16, nullptr, sl.x[size_t(l)], a.rstd1, w.attn_norm.p32, dxm, dxi, dxib,
-                  w.attn_norm.g32, int(M), int(H), coef_, stream);
+                  w.attn_norm.g32, int(M), int(H), stream);
     kcheck("rmsnorm_bwd");
   }
 
@@ -961,7 +958,7 @@ class Executor {
       gemm_kind_ = 0;
       tp_allreduce_bf16(dy16, M * H);
       k_rmsnorm_bwd(dy16, nullptr, sl.x[size_t(nl)], sl.rstdf, final_norm.p32, nullptr, cur, curb,
-                    final_norm.g32, int(M), int(H), coef_, stream);
+                    final_norm.g32, int(M), int(H), stream);
       kcheck("rmsnorm_bwd");
       group_ready(kGroupHead);
     } else {

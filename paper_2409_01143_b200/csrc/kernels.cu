@@ -21,10 +21,6 @@ inline int ew_grid(long long n, int per_thread) {
   return int(blocks);
 }
 
-inline int row_grid(int rows, int warps_per_block) {
-  return (rows + warps_per_block - 1) / warps_per_block;
-}
-
 __device__ __forceinline__ float bf(bf16 x) { return __bfloat162float(x); }
 
 // ------------------------------------------------------------------ init
@@ -89,140 +85,23 @@ __global__ void embed_bwd_kernel(const int32_t* tok, const float* dx, float* dE,
 }
 
 // ------------------------------------------------------------------ rmsnorm
-// one warp per row; H % 8 == 0
-__global__ void rmsnorm_fwd_kernel(const float* __restrict__ x, const bf16* __restrict__ y,
-                                   float* xo, const float* __restrict__ g, bf16* __restrict__ out,
-                                   float* __restrict__ rstd, int M, int H, float eps) {
-  int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  int lane = threadIdx.x % 32;
-  if (row >= M) return;
-  const float4* xr = reinterpret_cast<const float4*>(x + (long long)row * H);
-  float4* xor_ = reinterpret_cast<float4*>(xo + (long long)row * H);
-  const uint2* yr = y ? reinterpret_cast<const uint2*>(y + (long long)row * H) : nullptr;
-  float ss = 0.f;
-  for (int i = lane; i < H / 4; i += 32) {
-    float4 v = xr[i];
-    if (yr) {
-      uint2 w = yr[i];
-      __nv_bfloat162 a = *reinterpret_cast<__nv_bfloat162*>(&w.x);
-      __nv_bfloat162 b = *reinterpret_cast<__nv_bfloat162*>(&w.y);
-      v.x += __low2float(a);
-      v.y += __high2float(a);
-      v.z += __low2float(b);
-      v.w += __high2float(b);
-      xor_[i] = v;
-    }
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
-  }
-  ss = warp_sum(ss);
-  float r = rsqrtf(ss / float(H) + eps);
-  if (lane == 0) rstd[row] = r;
-  const float4* src = yr ? reinterpret_cast<const float4*>(xo + (long long)row * H) : xr;
-  const float4* g4 = reinterpret_cast<const float4*>(g);
-  uint2* o = reinterpret_cast<uint2*>(out + (long long)row * H);
-  for (int i = lane; i < H / 4; i += 32) {
-    float4 v = src[i];
-    float4 gg = g4[i];
-    uint2 w;
-    w.x = pack_bf16x2(v.x * r * gg.x, v.y * r * gg.y);
-    w.y = pack_bf16x2(v.z * r * gg.z, v.w * r * gg.w);
-    o[i] = w;
-  }
-}
+// Row-band kernels: a 256-thread CTA owns whole rows, each thread 8 columns
+// per 2048-column chunk (NC chunks cover H), so a row is read from HBM once
+// with every load of the row in flight together; the row statistic is a
+// block reduction through a double-buffered smem slot (one barrier per row).
+constexpr int kNormThreads = 256;
+constexpr int kNormChunk = kNormThreads * 8;
 
-__global__ void residual_add_kernel(const float* x, const bf16* y, float* xo, long long n) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    xo[i] = x[i] + bf(y[i]);
+__device__ __forceinline__ void load8f(const float* p, float* f) {
+  const float4 a = *reinterpret_cast<const float4*>(p);
+  const float4 b = *reinterpret_cast<const float4*>(p + 4);
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+  f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
 }
-
-// RMSNorm backward, two passes:
-//   (1) warp per row: c[m] = r^3/H * sum_j dy*g*x
-//   (2) column tiles (coalesced float4 columns x 64-row bands):
-//       dx = dres + r*dy*g - x*c ;  dg[j] += sum_rows dy*x*r  (register
-//       accumulation over the band, one atomic per column per band)
-template <bool kDyBf16>
-__device__ __forceinline__ float4 load_dy(const bf16* dyb, const float* dyf, long long off) {
-  if (kDyBf16) {
-    uint2 w = *reinterpret_cast<const uint2*>(dyb + off);
-    __nv_bfloat162 a = *reinterpret_cast<__nv_bfloat162*>(&w.x);
-    __nv_bfloat162 b = *reinterpret_cast<__nv_bfloat162*>(&w.y);
-    return make_float4(__low2float(a), __high2float(a), __low2float(b), __high2float(b));
-  }
-  return *reinterpret_cast<const float4*>(dyf + off);
+__device__ __forceinline__ void store8f(float* p, const float* f) {
+  *reinterpret_cast<float4*>(p) = make_float4(f[0], f[1], f[2], f[3]);
+  *reinterpret_cast<float4*>(p + 4) = make_float4(f[4], f[5], f[6], f[7]);
 }
-
-template <bool kDyBf16>
-__global__ void rmsnorm_bwd_dot_kernel(const bf16* __restrict__ dyb, const float* __restrict__ dyf,
-                                       const float* __restrict__ x, const float* __restrict__ rstd,
-                                       const float* __restrict__ g, float* __restrict__ coef,
-                                       int M, int H) {
-  int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  int lane = threadIdx.x % 32;
-  if (row >= M) return;
-  const long long base = (long long)row * H;
-  float dot = 0.f;
-  for (int i = lane * 4; i < H; i += 128) {
-    float4 xv = *reinterpret_cast<const float4*>(x + base + i);
-    float4 gv = *reinterpret_cast<const float4*>(g + i);
-    float4 d = load_dy<kDyBf16>(dyb, dyf, base + i);
-    dot += d.x * gv.x * xv.x + d.y * gv.y * xv.y + d.z * gv.z * xv.z + d.w * gv.w * xv.w;
-  }
-  dot = warp_sum(dot);
-  if (lane == 0) {
-    const float r = rstd[row];
-    coef[row] = dot * r * r * r / float(H);
-  }
-}
-
-template <bool kDyBf16>
-__global__ void rmsnorm_bwd_dx_kernel(const bf16* __restrict__ dyb, const float* __restrict__ dyf,
-                                      const float* __restrict__ x, const float* __restrict__ rstd,
-                                      const float* __restrict__ coef,
-                                      const float* __restrict__ g, const float* __restrict__ dres,
-                                      float* __restrict__ dx, bf16* __restrict__ dxb,
-                                      float* __restrict__ dg, int M, int H, int band) {
-  const int col = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
-  if (col >= H) return;
-  const int r0 = blockIdx.y * band;
-  const int r1 = min(M, r0 + band);
-  const float4 gv = *reinterpret_cast<const float4*>(g + col);
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int row = r0; row < r1; ++row) {
-    const long long off = (long long)row * H + col;
-    const float r = rstd[row];
-    const float c = coef[row];
-    float4 xv = *reinterpret_cast<const float4*>(x + off);
-    float4 d = load_dy<kDyBf16>(dyb, dyf, off);
-    acc.x += d.x * xv.x * r;
-    acc.y += d.y * xv.y * r;
-    acc.z += d.z * xv.z * r;
-    acc.w += d.w * xv.w * r;
-    float4 o;
-    o.x = r * d.x * gv.x - xv.x * c;
-    o.y = r * d.y * gv.y - xv.y * c;
-    o.z = r * d.z * gv.z - xv.z * c;
-    o.w = r * d.w * gv.w - xv.w * c;
-    if (dres) {
-      float4 rv = *reinterpret_cast<const float4*>(dres + off);
-      o.x += rv.x; o.y += rv.y; o.z += rv.z; o.w += rv.w;
-    }
-    *reinterpret_cast<float4*>(dx + off) = o;
-    if (dxb) {
-      uint2 w;
-      w.x = pack_bf16x2(o.x, o.y);
-      w.y = pack_bf16x2(o.z, o.w);
-      *reinterpret_cast<uint2*>(dxb + off) = w;
-    }
-  }
-  atomicAdd(dg + col + 0, acc.x);
-  atomicAdd(dg + col + 1, acc.y);
-  atomicAdd(dg + col + 2, acc.z);
-  atomicAdd(dg + col + 3, acc.w);
-}
-
-// ------------------------------------------------------------------ rope
-// thread per (row, head, i < d/2) pair, applied to q and k
 __device__ __forceinline__ void unpack8(uint4 w, float* f) {
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
 #pragma unroll
@@ -231,7 +110,6 @@ __device__ __forceinline__ void unpack8(uint4 w, float* f) {
     f[2 * k + 1] = __high2float(h[k]);
   }
 }
-
 __device__ __forceinline__ uint4 pack8(const float* f) {
   uint4 w;
   w.x = pack_bf16x2(f[0], f[1]);
@@ -241,38 +119,261 @@ __device__ __forceinline__ uint4 pack8(const float* f) {
   return w;
 }
 
-// thread per (row, head, q|k, 8 rotation pairs): 16-byte loads of both halves
+// sum over the CTA; red is [2][8] floats, parity alternates per row
+__device__ __forceinline__ float norm_block_sum(float v, float* red, int parity) {
+  v = warp_sum(v);
+  const int w = threadIdx.x / 32;
+  if ((threadIdx.x & 31) == 0) red[parity * 8 + w] = v;
+  __syncthreads();
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < kNormThreads / 32; ++i) s += red[parity * 8 + i];
+  return s;
+}
+
+template <int NC>
+__global__ void __launch_bounds__(kNormThreads)
+    rmsnorm_fwd_kernel(const float* __restrict__ x, const bf16* __restrict__ y, float* xo,
+                       const float* __restrict__ g, bf16* __restrict__ out,
+                       float* __restrict__ rstd, int M, int H, float eps) {
+  __shared__ float red[16];
+  float gr[NC][8];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int col = c * kNormChunk + threadIdx.x * 8;
+    if (col < H) load8f(g + col, gr[c]);
+  }
+  int parity = 0;
+  for (int row = blockIdx.x; row < M; row += gridDim.x, parity ^= 1) {
+    const long long base = (long long)row * H;
+    float v[NC][8];
+    float ss = 0.f;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int col = c * kNormChunk + threadIdx.x * 8;
+      if (col < H) {
+        load8f(x + base + col, v[c]);
+        if (y) {
+          float t[8];
+          unpack8(*reinterpret_cast<const uint4*>(y + base + col), t);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[c][k] += t[k];
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) ss += v[c][k] * v[c][k];
+      }
+    }
+    ss = norm_block_sum(ss, red, parity);
+    const float r = rsqrtf(ss / float(H) + eps);
+    if (threadIdx.x == 0) rstd[row] = r;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int col = c * kNormChunk + threadIdx.x * 8;
+      if (col < H) {
+        if (y) store8f(xo + base + col, v[c]);
+        float o[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[k] = v[c][k] * r * gr[c][k];
+        *reinterpret_cast<uint4*>(out + base + col) = pack8(o);
+      }
+    }
+  }
+}
+
+__global__ void residual_add_kernel(const float* x, const bf16* y, float* xo, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    xo[i] = x[i] + bf(y[i]);
+}
+
+// RMSNorm backward, one pass; a persistent CTA per SM walks rows
+// blockIdx.x, +grid, ... through a ring of shared-memory stages filled by
+// 1-D bulk copies (x, dy, dres of one row per stage):
+//   c   = r^3/H * sum_j dy*g*x            (block reduction per row)
+//   dx  = dres + r*dy*g - x*c
+//   dg += sum_rows dy*x*r                 (registers over the CTA's rows,
+//                                          one atomic per column per CTA)
+// Stage reuse needs no extra barrier: the per-row reduction barrier of row k
+// proves every thread has finished row k-1, whose stage is refilled then.
+// Thread t owns columns c*2048 + q*1024 + 4t .. +3 (q = 0, 1): conflict-free
+// 16-byte shared reads and coalesced global stores.
+constexpr int kNormStages = 4;
+
+template <int NC, bool kDyBf16>
+__global__ void __launch_bounds__(kNormThreads, NC <= 2 ? 2 : 1)
+    rmsnorm_bwd_kernel(const bf16* __restrict__ dyb, const float* __restrict__ dyf,
+                       const float* __restrict__ x, const float* __restrict__ rstd,
+                       const float* __restrict__ g, const float* dres, float* dx,
+                       bf16* __restrict__ dxb, float* __restrict__ dg, int M, int H, int nst) {
+  extern __shared__ uint8_t nsm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(nsm_raw) + 127) & ~uintptr_t(127));
+  __shared__ float red[16];
+  __shared__ __align__(8) uint64_t full[kNormStages];
+  const uint32_t xb = uint32_t(H) * 4, yb = uint32_t(H) * (kDyBf16 ? 2 : 4);
+  const uint32_t rb = dres ? uint32_t(H) * 4 : 0;
+  const uint32_t stage_bytes = xb + yb + rb;
+  const int G = gridDim.x;
+  const int nrows = blockIdx.x < M ? (M - 1 - int(blockIdx.x)) / G + 1 : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int k) {
+    const long long row = blockIdx.x + (long long)k * G;
+    const int s = k % nst;
+    uint8_t* st = sm + size_t(s) * stage_bytes;
+    mbar_arrive_expect_tx(&full[s], stage_bytes);
+    bulk_load_1d(st, x + row * H, xb, &full[s]);
+    if (kDyBf16)
+      bulk_load_1d(st + xb, dyb + row * H, yb, &full[s]);
+    else
+      bulk_load_1d(st + xb, dyf + row * H, yb, &full[s]);
+    if (dres) bulk_load_1d(st + xb + yb, dres + row * H, rb, &full[s]);
+  };
+  if (threadIdx.x == 0)
+    for (int k = 0; k < nst && k < nrows; ++k) issue(k);
+
+  float gr[NC][8], acc[NC][8];
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int col = c * kNormChunk + q * (kNormChunk / 2) + threadIdx.x * 4;
+      if (col < H) {
+        const float4 v = *reinterpret_cast<const float4*>(g + col);
+        gr[c][4 * q] = v.x; gr[c][4 * q + 1] = v.y; gr[c][4 * q + 2] = v.z; gr[c][4 * q + 3] = v.w;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[c][4 * q + k] = 0.f;
+    }
+
+  float r_next = nrows > 0 ? rstd[blockIdx.x] : 0.f;
+  for (int k = 0; k < nrows; ++k) {
+    const long long row = blockIdx.x + (long long)k * G;
+    const long long base = row * H;
+    const float r = r_next;
+    if (k + 1 < nrows) r_next = rstd[row + G];  // one row ahead: off the critical path
+    const int s = k % nst;
+    const uint8_t* st = sm + size_t(s) * stage_bytes;
+    const float* sx = reinterpret_cast<const float*>(st);
+    const float* sres = reinterpret_cast<const float*>(st + xb + yb);
+    mbar_wait(&full[s], uint32_t(k / nst) & 1u);
+    float xv[NC][8], dv[NC][8];
+    float dot = 0.f;
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int col = c * kNormChunk + q * (kNormChunk / 2) + threadIdx.x * 4;
+        if (col < H) {
+          const float4 xx = lds_f4(sx + col);
+          float d4[4];
+          if (kDyBf16) {
+            const uint2 w = lds_u2(st + xb + size_t(col) * 2);
+            const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&w.x);
+            const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&w.y);
+            d4[0] = __low2float(a); d4[1] = __high2float(a);
+            d4[2] = __low2float(b); d4[3] = __high2float(b);
+          } else {
+            const float4 v = lds_f4(st + xb + size_t(col) * 4);
+            d4[0] = v.x; d4[1] = v.y; d4[2] = v.z; d4[3] = v.w;
+          }
+          const float x4[4] = {xx.x, xx.y, xx.z, xx.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            xv[c][4 * q + e] = x4[e];
+            dv[c][4 * q + e] = d4[e];
+            dot += d4[e] * gr[c][4 * q + e] * x4[e];
+            acc[c][4 * q + e] += d4[e] * x4[e] * r;
+          }
+        }
+      }
+    dot = norm_block_sum(dot, red, k & 1);
+    if (threadIdx.x == 0 && k >= 1 && k - 1 + nst < nrows) issue(k - 1 + nst);
+    const float cf = dot * r * r * r / float(H);
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int col = c * kNormChunk + q * (kNormChunk / 2) + threadIdx.x * 4;
+        if (col < H) {
+          float o[4];
+          if (dres) {
+            const float4 v = lds_f4(sres + col);
+            o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+          } else {
+            o[0] = o[1] = o[2] = o[3] = 0.f;
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            o[e] += r * dv[c][4 * q + e] * gr[c][4 * q + e] - xv[c][4 * q + e] * cf;
+          *reinterpret_cast<float4*>(dx + base + col) = make_float4(o[0], o[1], o[2], o[3]);
+          if (dxb) {
+            uint2 w;
+            w.x = pack_bf16x2(o[0], o[1]);
+            w.y = pack_bf16x2(o[2], o[3]);
+            *reinterpret_cast<uint2*>(dxb + base + col) = w;
+          }
+        }
+      }
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int col = c * kNormChunk + q * (kNormChunk / 2) + threadIdx.x * 4;
+      if (col < H) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) atomicAdd(dg + col + e, acc[c][4 * q + e]);
+      }
+    }
+}
+
+// ------------------------------------------------------------------ rope
+// thread per (row, group of kRopeHeads heads, 8 rotation pairs): the 8
+// sin/cos pairs are computed once and applied to q and k of every head in
+// the group; 16-byte loads of both halves, all loads of the group in flight
+constexpr int kRopeHeads = 4;
 __global__ void rope_kernel(bf16* qkv, int M, int S, int nh, int d, float theta, int inverse) {
   const int half = d / 2;
   const int g8 = half / 8;
+  const int ng = (nh + kRopeHeads - 1) / kRopeHeads;
   const float l2t = log2f(theta);
-  long long n = (long long)M * nh * 2 * g8;
+  long long n = (long long)M * ng * g8;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
        idx += (long long)gridDim.x * blockDim.x) {
     const int i8 = int(idx % g8);
     long long t = idx / g8;
-    const int part = int(t % 2);
-    t /= 2;
-    const int h = int(t % nh);
-    const int row = int(t / nh);
+    const int hg = int(t % ng);
+    const int row = int(t / ng);
     const float pos = float(row % S);
-    bf16* base = qkv + (long long)row * nh * 3 * d + (long long)h * 3 * d + part * d + i8 * 8;
-    float a[8], b[8];
-    unpack8(*reinterpret_cast<const uint4*>(base), a);
-    unpack8(*reinterpret_cast<const uint4*>(base + half), b);
+    float sn[8], cs[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int i = i8 * 8 + k;
       const float inv_freq = exp2f(-2.0f * float(i) / float(d) * l2t);
-      float sn, cs;
-      sincosf(pos * inv_freq, &sn, &cs);
-      if (inverse) sn = -sn;
-      const float x = a[k], y = b[k];
-      a[k] = x * cs - y * sn;
-      b[k] = y * cs + x * sn;
+      sincosf(pos * inv_freq, &sn[k], &cs[k]);
+      if (inverse) sn[k] = -sn[k];
     }
-    *reinterpret_cast<uint4*>(base) = pack8(a);
-    *reinterpret_cast<uint4*>(base + half) = pack8(b);
+    bf16* rbase = qkv + (long long)row * nh * 3 * d + i8 * 8;
+#pragma unroll
+    for (int j = 0; j < 2 * kRopeHeads; ++j) {
+      const int h = hg * kRopeHeads + j / 2;
+      if (h >= nh) break;
+      bf16* base = rbase + (long long)h * 3 * d + (j & 1) * d;
+      float a[8], b[8];
+      unpack8(*reinterpret_cast<const uint4*>(base), a);
+      unpack8(*reinterpret_cast<const uint4*>(base + half), b);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float x = a[k], y = b[k];
+        a[k] = x * cs[k] - y * sn[k];
+        b[k] = y * cs[k] + x * sn[k];
+      }
+      *reinterpret_cast<uint4*>(base) = pack8(a);
+      *reinterpret_cast<uint4*>(base + half) = pack8(b);
+    }
   }
 }
 
@@ -373,14 +474,20 @@ __global__ void ce_stats_kernel(const float* __restrict__ logits, int Vr, int v0
   int row = blockIdx.x;
   const float* l = logits + (long long)row * Vr;
   float mx = -FLT_MAX, sm = 0.f;
-  for (int j = threadIdx.x; j < Vr; j += blockDim.x) {
-    float v = l[j];
-    if (v > mx) {
-      sm = sm * __expf(mx - v) + 1.f;
-      mx = v;
-    } else {
-      sm += __expf(v - mx);
+  // 8 logits per step (two float4, Vr % 64 == 0): one rescale per 8 values
+  const float4* l4 = reinterpret_cast<const float4*>(l);
+  for (int j = threadIdx.x; j < Vr / 8; j += blockDim.x) {
+    const float4 a = l4[2 * j], b = l4[2 * j + 1];
+    const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    float m8 = v[0];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) m8 = fmaxf(m8, v[k]);
+    if (m8 > mx) {
+      sm *= __expf(mx - m8);
+      mx = m8;
     }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sm += __expf(v[k] - mx);
   }
   // combine (mx, sm) across the block
   __shared__ float smx[32], ssm[32];
@@ -428,10 +535,16 @@ __global__ void ce_finish_kernel(const float* __restrict__ logits, int Vr, int v
   float m = gmax[row];
   float inv_s = 1.f / st2[2 * row];
   int t = target_of(tok, row, S) - v0;
-  for (int j = threadIdx.x; j < Vr; j += blockDim.x) {
-    float p = __expf(l[j] - m) * inv_s;
-    if (j == t) p -= 1.f;
-    d[j] = __float2bfloat16_rn(p * inv_count);
+  const float4* l4 = reinterpret_cast<const float4*>(l);
+  for (int j = threadIdx.x; j < Vr / 4; j += blockDim.x) {
+    const float4 a = l4[j];
+    float p[4] = {__expf(a.x - m) * inv_s, __expf(a.y - m) * inv_s, __expf(a.z - m) * inv_s,
+                  __expf(a.w - m) * inv_s};
+    if (t >= 4 * j && t < 4 * j + 4) p[t - 4 * j] -= 1.f;
+    uint2 w;
+    w.x = pack_bf16x2(p[0] * inv_count, p[1] * inv_count);
+    w.y = pack_bf16x2(p[2] * inv_count, p[3] * inv_count);
+    *reinterpret_cast<uint2*>(d + 4 * j) = w;
   }
   if (threadIdx.x == 0 && v0 == 0) {
     // loss counted once per row, on the rank owning vocab offset 0
@@ -555,30 +668,63 @@ void k_embed_bwd(const int32_t* tok, const float* dx, float* dE, int M, int S, i
                  cudaStream_t s) {
   if (M > 0) embed_bwd_kernel<<<M, 256, 0, s>>>(tok, dx, dE, M, S, H);
 }
+// H <= 4 * 2048 (checked by the executor's model validation)
 void k_rmsnorm_fwd(const float* x, const bf16* y, float* xo, const float* g, bf16* out,
                    float* rstd, int M, int H, float eps, cudaStream_t s) {
-  if (M > 0) rmsnorm_fwd_kernel<<<row_grid(M, 8), 256, 0, s>>>(x, y, xo, g, out, rstd, M, H, eps);
+  if (M <= 0) return;
+  const int grid = std::min(M, 148 * 8);
+  const int nc = (H + kNormChunk - 1) / kNormChunk;
+#define HX_NORM_FWD(NC) \
+  rmsnorm_fwd_kernel<NC><<<grid, kNormThreads, 0, s>>>(x, y, xo, g, out, rstd, M, H, eps)
+  if (nc <= 1) HX_NORM_FWD(1);
+  else if (nc == 2) HX_NORM_FWD(2);
+  else if (nc == 3) HX_NORM_FWD(3);
+  else HX_NORM_FWD(4);
+#undef HX_NORM_FWD
 }
 void k_residual_add(const float* x, const bf16* y, float* xo, long long n, cudaStream_t s) {
   if (n > 0) residual_add_kernel<<<ew_grid(n, 4), 256, 0, s>>>(x, y, xo, n);
 }
 void k_rmsnorm_bwd(const bf16* dyb, const float* dyf, const float* x, const float* rstd,
                    const float* g, const float* dres, float* dx, bf16* dxb, float* dg, int M,
-                   int H, float* coef, cudaStream_t s) {
+                   int H, cudaStream_t s) {
   if (M <= 0) return;
-  const int band = 16;  // rows per block: enough blocks in flight to cover HBM latency
-  dim3 g2((H / 4 + 127) / 128, (M + band - 1) / band);
+  // persistent CTAs (two per SM while H <= 4096 so one CTA's row barrier
+  // overlaps the other's copies); each CTA's rows end in one dg atomic per column
+  const int nc = (H + kNormChunk - 1) / kNormChunk;
+  const int per_sm = 1;
+  const int grid = std::min(M, kNumSmsHint * per_sm);
+  const size_t stage = size_t(H) * (4 + (dyb ? 2 : 4) + (dres ? 4 : 0));
+  const size_t budget = per_sm == 2 ? (100u << 10) : (200u << 10);
+  const int nst = int(std::max<size_t>(1, std::min<size_t>(kNormStages, budget / stage)));
+  const size_t smem = stage * nst + 128;
+#define HX_NORM_BWD(NC, B)                                                                   \
+  do {                                                                                      \
+    static bool attr = false;                                                               \
+    if (!attr) {                                                                            \
+      cudaFuncSetAttribute(rmsnorm_bwd_kernel<NC, B>,                                       \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 210 << 10);         \
+      attr = true;                                                                          \
+    }                                                                                       \
+    rmsnorm_bwd_kernel<NC, B><<<grid, kNormThreads, smem, s>>>(dyb, dyf, x, rstd, g, dres, dx, \
+                                                                dxb, dg, M, H, nst);        \
+  } while (0)
+#define HX_NORM_BWD_NC(B)       \
+  if (nc <= 1) HX_NORM_BWD(1, B); \
+  else if (nc == 2) HX_NORM_BWD(2, B); \
+  else if (nc == 3) HX_NORM_BWD(3, B); \
+  else HX_NORM_BWD(4, B);
   if (dyb) {
-    rmsnorm_bwd_dot_kernel<true><<<row_grid(M, 8), 256, 0, s>>>(dyb, dyf, x, rstd, g, coef, M, H);
-    rmsnorm_bwd_dx_kernel<true><<<g2, 128, 0, s>>>(dyb, dyf, x, rstd, coef, g, dres, dx, dxb, dg, M, H, band);
+    HX_NORM_BWD_NC(true)
   } else {
-    rmsnorm_bwd_dot_kernel<false><<<row_grid(M, 8), 256, 0, s>>>(dyb, dyf, x, rstd, g, coef, M, H);
-    rmsnorm_bwd_dx_kernel<false><<<g2, 128, 0, s>>>(dyb, dyf, x, rstd, coef, g, dres, dx, dxb, dg, M, H, band);
+    HX_NORM_BWD_NC(false)
   }
+#undef HX_NORM_BWD_NC
+#undef HX_NORM_BWD
 }
 void k_rope(bf16* qkv, int M, int S, int nh, int d, float theta, int inverse, cudaStream_t s) {
-  long long n = (long long)M * nh * (d / 2);
-  if (n > 0) rope_kernel<<<ew_grid(n, 4), 256, 0, s>>>(qkv, M, S, nh, d, theta, inverse);
+  long long n = (long long)M * ((nh + kRopeHeads - 1) / kRopeHeads) * (d / 16);
+  if (n > 0) rope_kernel<<<ew_grid(n, 1), 256, 0, s>>>(qkv, M, S, nh, d, theta, inverse);
 }
 void k_softmax_fwd(const float* S, bf16* P, int L, int nb, cudaStream_t s) {
   long long rows = (long long)L * nb;

@@ -72,11 +72,11 @@ void k_rmsnorm_fwd(const float* x, const bf16* y, float* xo, const float* g, bf1
 void k_residual_add(const float* x, const bf16* y, float* xo, long long n, cudaStream_t s);
 // dx = dres + rmsnorm_bwd(dy);  dx_bf16 optional copy;  dg += sum_m dy*xhat
 // dy is bf16 if dy_bf16 != null else fp32 (dy_f32)
-// coef: [M] fp32 scratch.  Safe in place (dx == dres): each element is read then
-// written by the same thread.
+// Safe in place (dx == dres): each element is read then written by the same
+// thread.
 void k_rmsnorm_bwd(const bf16* dy_bf16, const float* dy_f32, const float* x, const float* rstd,
                    const float* g, const float* dres, float* dx, bf16* dx_bf16, float* dg, int M,
-                   int H, float* coef, cudaStream_t s);
+                   int H, cudaStream_t s);
 
 // in-place rotary embedding of q and k inside the fused [M, nh*3*d] buffer
 // (rotate-half convention); inverse=1 applies the transpose (backward).
