@@ -124,6 +124,10 @@ hexexec_status hexexec_k_gemm(int M, int N, int K, int nb1, int nb2, const void*
                               int64_t ldb, int64_t b_bs1, int64_t b_bs2, void* C, int64_t ldc,
                               int64_t c_bs1, int64_t c_bs2, int c_fp32, int beta, float alpha,
                               int causal, void* stream);
+/* tail split-K of later hexexec_k_gemm calls: split -1 auto, 0 off, >1 force
+ * that many k-parts; ws (fp32, ws_bytes) and counters (n ints) must be zeroed
+ * device memory, or NULL (then only beta GEMMs without workspace split). */
+hexexec_status hexexec_k_gemm_split(int split, float* ws, size_t ws_bytes, int* counters, int n);
 /* fused causal attention over the head-interleaved QKV buffer [mb*S, nh*3*d]:
  * out [mb*S, nh*d] bf16, lse [mb*nh, S] (log2 domain); backward writes
  * dq/dk/dv into dqkv [mb*S, nh*3*d] (delta / dq_acc: fp32 scratch of

@@ -254,6 +254,17 @@ char* hexexec_stats_json(const hexexec_ctx* ctx) {
 }
 
 // ------------------------------------------------------------------ kernels
+namespace {
+struct KSplit {
+  int split;
+  float* ws;
+  size_t ws_bytes;
+  int* cnt;
+  int n;
+};
+KSplit g_k_split = {-1, nullptr, 0, nullptr, 0};
+}  // namespace
+
 hexexec_status hexexec_k_gemm(int M, int N, int K, int nb1, int nb2, const void* A, int a_mn,
                               int64_t lda, int64_t a_bs1, int64_t a_bs2, const void* B, int b_mn,
                               int64_t ldb, int64_t b_bs1, int64_t b_bs2, void* C, int64_t ldc,
@@ -275,7 +286,17 @@ hexexec_status hexexec_k_gemm(int M, int N, int K, int nb1, int nb2, const void*
   d.beta = beta;
   d.alpha = alpha;
   d.causal = causal;
+  d.split = g_k_split.split;
+  d.ws = g_k_split.ws;
+  d.ws_bytes = g_k_split.ws_bytes;
+  d.ws_cnt = g_k_split.cnt;
+  d.ws_cnt_n = g_k_split.n;
   return cuda_status(hexexec::gemm_bf16(d, as_stream(stream)));
+}
+
+hexexec_status hexexec_k_gemm_split(int split, float* ws, size_t ws_bytes, int* counters, int n) {
+  g_k_split = {split, ws, ws_bytes, counters, n};
+  return HEXEXEC_OK;
 }
 
 hexexec_status hexexec_k_attn_fwd(const void* qkv, void* out, float* lse, int S, int nh, int d,
@@ -323,8 +344,19 @@ hexexec_status hexexec_k_rmsnorm_bwd(const void* dyb, const float* dyf, const fl
                                      const float* rstd, const float* g, const float* dres,
                                      float* dx, void* dxb, float* dg, int M, int H,
                                      void* stream) {
+  // partial-dg scratch kept across calls (grown on demand; kernel entry only)
+  static float* part = nullptr;
+  static size_t cap = 0;
+  const size_t need = size_t(hexexec::kRmsBwdCtas) * size_t(H > 0 ? H : 1) * sizeof(float);
+  if (need > cap) {
+    if (part) cudaFree(part);
+    part = nullptr;
+    cap = 0;
+    if (cudaMalloc(&part, need) != cudaSuccess) return HEXEXEC_ERR_CUDA;
+    cap = need;
+  }
   hexexec::k_rmsnorm_bwd(static_cast<const hexexec::bf16*>(dyb), dyf, x, rstd, g, dres, dx,
-                         static_cast<hexexec::bf16*>(dxb), dg, M, H, as_stream(stream));
+                         static_cast<hexexec::bf16*>(dxb), dg, M, H, part, as_stream(stream));
   return cuda_status(cudaGetLastError());
 }
 

@@ -73,6 +73,7 @@ ExecConfig parse_exec_config(const std::string& text) {
       else if (k == "cuda_graph") c.cuda_graph = v.get<bool>();
       else if (k == "attention") c.attention = v.get<std::string>();
       else if (k == "dp_overlap") c.dp_overlap = v.get<bool>();
+      else if (k == "gemm_split") c.gemm_split = v.get<bool>();
       else throw ParseError("exec config: unknown key '" + k + "'");
     } catch (const nlohmann::json::exception& e) {
       throw ParseError("exec config: bad value for '" + k + "'");
@@ -193,6 +194,9 @@ class Executor {
   float *dx[2] = {nullptr, nullptr}, *ce_scr = nullptr, *loss_acc = nullptr, *loss_host = nullptr;
   bf16* dxb = nullptr;
   float *delta_ = nullptr, *dq_acc_ = nullptr;
+  float* gemm_ws_ = nullptr;  // zero between GEMMs (the kernel leaves it zero)
+  int* gemm_cnt_ = nullptr;
+  float* dg_part_ = nullptr;
   int32_t* tokens = nullptr;
   int32_t* tokens_pinned = nullptr;
   float* idle_loss_ = nullptr;
@@ -446,6 +450,9 @@ class Executor {
     arena.reserve(M * H * 4 * 2 + M * H * 2 + M * H * 2);  // dx ping-pong, dxb, dy16
     if (role.last_stage) arena.reserve(M * Vr * 4 + 5 * M * 4);
     arena.reserve(256);                                    // loss
+    arena.reserve(kGemmWsBytes);                           // GEMM tail-split workspace
+    arena.reserve(kGemmWsCounters * 4);
+    arena.reserve(size_t(kRmsBwdCtas) * H * 4);             // rmsnorm bwd partial dg rows
     arena.reserve(role.batch * (S + 1) * 4);               // tokens
     if (cfg.validate_only) return;
     arena.commit();
@@ -485,6 +492,9 @@ class Executor {
     dS = arena.take<bf16>(SS);
     delta_ = arena.take<float>(LSE);
     dq_acc_ = arena.take<float>(M * kr);
+    gemm_ws_ = arena.take<float>(kGemmWsBytes / 4);
+    gemm_cnt_ = arena.take<int>(kGemmWsCounters);
+    dg_part_ = arena.take<float>(size_t(kRmsBwdCtas) * H);
     ypart = arena.take<bf16>(M * H);
     da = arena.take<bf16>(M * F);
     dgu = arena.take<bf16>(M * 2 * F);
@@ -501,6 +511,8 @@ class Executor {
     loss_acc = arena.take<float>(32);
     sp_ = reinterpret_cast<StepParams*>(loss_acc + 16);
     HX_CUDA(cudaMemsetAsync(sp_, 0, sizeof(StepParams), stream));
+    HX_CUDA(cudaMemsetAsync(gemm_ws_, 0, kGemmWsBytes, stream));
+    HX_CUDA(cudaMemsetAsync(gemm_cnt_, 0, kGemmWsCounters * sizeof(int), stream));
     tokens = arena.take<int32_t>(role.batch * (S + 1));
     HX_CUDA(cudaMallocHost(&tokens_pinned, size_t(role.batch * (S + 1)) * 4));
     HX_CUDA(cudaMallocHost(&loss_host, 64));
@@ -613,7 +625,13 @@ class Executor {
   double gemm_ms_[3] = {0, 0, 0}, gemm_flops_[3] = {0, 0, 0};
   int64_t gemm_count_[3] = {0, 0, 0};
 
-  void gemm(const GemmDesc& g) {
+  void gemm(const GemmDesc& gin) {
+    GemmDesc g = gin;
+    g.split = cfg.gemm_split ? -1 : 0;
+    g.ws = gemm_ws_;
+    g.ws_bytes = kGemmWsBytes;
+    g.ws_cnt = gemm_cnt_;
+    g.ws_cnt_n = kGemmWsCounters;
     GemmRec* rec = nullptr;
     if (cfg.profile_gemm) {
       if (gemm_used_ == gemm_pool_.size()) {
@@ -845,7 +863,7 @@ class Executor {
     float* dxm = dxi;
     bf16* dxmb = dxib;
     k_rmsnorm_bwd(dy16, nullptr, a.x_mid, a.rstd2, w.mlp_norm.p32, dxo, dxm, dxmb, w.mlp_norm.g32,
-                  int(M), int(H), stream);
+                  int(M), int(H), dg_part_, stream);
     kcheck("rmsnorm_bwd");
     // attention: O projection
     gemm(g2(M, kr, H, dxmb, 0, H, w.wo.p16, 0, H, dattn, kr, 0));
@@ -866,7 +884,7 @@ class Executor {
     tp_allreduce_bf16(dy16, M * H);
     // dx_in = dx_mid + rmsnorm_bwd(dxn): in place over dx_mid (row-local)
     k_rmsnorm_bwd(dy16, nullptr, sl.x[size_t(l)], a.rstd1, w.attn_norm.p32, dxm, dxi, dxib,
-                  w.attn_norm.g32, int(M), int(H), stream);
+                  w.attn_norm.g32, int(M), int(H), dg_part_, stream);
     kcheck("rmsnorm_bwd");
   }
 
@@ -958,7 +976,7 @@ class Executor {
       gemm_kind_ = 0;
       tp_allreduce_bf16(dy16, M * H);
       k_rmsnorm_bwd(dy16, nullptr, sl.x[size_t(nl)], sl.rstdf, final_norm.p32, nullptr, cur, curb,
-                    final_norm.g32, int(M), int(H), stream);
+                    final_norm.g32, int(M), int(H), dg_part_, stream);
       kcheck("rmsnorm_bwd");
       group_ready(kGroupHead);
     } else {

@@ -21,6 +21,10 @@ struct ExecConfig {
   bool cuda_graph = true;             // replay the captured step graph (after step 0)
   std::string attention = "fused";    // "fused" (flash, tcgen05) | "unfused" (GEMM+softmax)
   bool dp_overlap = true;             // DP sync + AdamW per layer on a second stream
+  // split-K of each GEMM's partial last wave (+3-7% on the affected GEMMs,
+  // ~1% of the step); partial sums land in arbitrary order, so it costs
+  // run-to-run bitwise determinism and is opt-in
+  bool gemm_split = false;
 };
 
 ExecConfig parse_exec_config(const std::string& text);

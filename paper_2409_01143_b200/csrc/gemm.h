@@ -42,7 +42,22 @@ struct GemmDesc {
   int beta = 0;    // 1: C += alpha*acc (fp32 C only)
   float alpha = 1.f;
   int causal = kCausalNone;
+  // Split-K of the last, partial wave of tiles (wave quantisation): the
+  // leftover tiles are cut into `s` k-ranges spread over all CTA pairs.
+  // beta GEMMs without R reduce-add their partials straight into C; the
+  // others reduce-add into the fp32 workspace `ws` and the last arriving
+  // partial (per-slab counter in `ws_cnt`) finishes the tile.  ws / ws_cnt
+  // must be zero on entry and are left zero.  split: -1 auto, 0 off, >1 force.
+  float* ws = nullptr;
+  size_t ws_bytes = 0;
+  int* ws_cnt = nullptr;
+  int ws_cnt_n = 0;
+  int split = -1;
 };
+
+// workspace a GemmDesc needs for any split (bytes, counters)
+constexpr size_t kGemmWsBytes = size_t(148) * 128 * 256 * 4;
+constexpr int kGemmWsCounters = 148 * 8;
 
 // Launch on `stream`.  Returns cudaSuccess or the launch error.  Tensor maps
 // are encoded on the host per call (cheap, ~1 us) from the descriptor.

@@ -42,6 +42,11 @@ struct EpiParams {
   float alpha;
   int causal;
   int m_tiles, n_tiles, num_tiles;
+  // split-K of the tail: tiles >= split_first are cut into split_s k-ranges
+  int split_first, split_s, num_units;
+  int split_direct;  // partials reduce-add straight into C (beta, no R)
+  float* ws;         // [split tiles][TM][BN] fp32
+  int* ws_cnt;       // per (split tile, 32-row slab)
 };
 
 template <int BN, int CG>
@@ -88,6 +93,33 @@ HX_DEVICE void k_range(const EpiParams& p, int m0, int& kb0, int& kb1) {
   if (kb1 < kb0) kb1 = kb0;
 }
 
+// work unit -> (tile, k part); part -1 = whole tile
+HX_DEVICE void decode_unit(const EpiParams& p, int u, int& t, int& part) {
+  if (u < p.split_first) {
+    t = u;
+    part = -1;
+  } else {
+    const int v = u - p.split_first;
+    t = p.split_first + v / p.split_s;
+    part = v % p.split_s;
+  }
+}
+
+template <int TM>
+HX_DEVICE void unit_k_range(const EpiParams& p, int m0, int part, int& kb0, int& kb1) {
+  k_range<TM>(p, m0, kb0, kb1);
+  if (part >= 0) {
+    const int len = kb1 - kb0;
+    const int a = kb0 + len * part / p.split_s;
+    kb1 = kb0 + len * (part + 1) / p.split_s;
+    kb0 = a;
+  }
+}
+
+HX_DEVICE void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // tile t -> (m0, n-tile index, batch coords); n fastest so CTAs of one wave
 // share the A row-panel in L2
 template <int TM>
@@ -100,11 +132,32 @@ HX_DEVICE void decode_tile(const EpiParams& p, int t, int& m0, int& nt, int& z1,
   z2 = z / p.nb1;
 }
 
+// stage a 32-row x 32-col chunk for TMA: fp32 rows of 128 B (SWIZZLE_128B) or
+// bf16 rows of 64 B (SWIZZLE_64B); lane = row
+HX_DEVICE void stage_chunk(uint8_t* sbuf, const float* v, bool f32, int lane) {
+  if (f32) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      *reinterpret_cast<float4*>(sbuf + swz<128>(lane, q)) =
+          make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 w;
+      w.x = pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+      w.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+      w.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+      w.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+      *reinterpret_cast<uint4*>(sbuf + swz<64>(lane, q)) = w;
+    }
+  }
+}
+
 template <int BN, int A_MN, int B_MN, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmR,
-                const EpiParams p) {
+                const __grid_constant__ CUtensorMap tmW, const EpiParams p) {
   using C = Cfg<BN, CG>;
   constexpr int ST = C::STAGES;
   constexpr int TM = C::TM;
@@ -165,13 +218,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---------------- TMA producer (both CTAs of a pair)
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = pid; t < p.num_tiles; t += npairs) {
+      for (int u = pid; u < p.num_units; u += npairs) {
+        int t, part;
+        decode_unit(p, u, t, part);
         int m0, nt, z1, z2;
         decode_tile<TM>(p, t, m0, nt, z1, z2);
         int n0 = nt * BN;
         if (tile_skipped<TM>(p, m0, n0)) continue;
         int kb0, kb1;
-        k_range<TM>(p, m0, kb0, kb1);
+        unit_k_range<TM>(p, m0, part, kb0, kb1);
         const int am = m0 + BM * int(crank);      // this CTA's A rows
         const int bn = n0 + C::BNC * int(crank);  // this CTA's B rows
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -228,13 +283,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = pid; t < p.num_tiles; t += npairs) {
+      for (int u = pid; u < p.num_units; u += npairs) {
+        int t, part;
+        decode_unit(p, u, t, part);
         int m0, nt, z1, z2;
         decode_tile<TM>(p, t, m0, nt, z1, z2);
         int n0 = nt * BN;
         if (tile_skipped<TM>(p, m0, n0)) continue;
         int kb0, kb1;
-        k_range<TM>(p, m0, kb0, kb1);
+        unit_k_range<TM>(p, m0, part, kb0, kb1);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t dtm = tbase + uint32_t(acc * BN);
@@ -283,14 +340,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0, rphase = 0;
     int sb = 0;
-    for (int t = pid; t < p.num_tiles; t += npairs) {
+    for (int u = pid; u < p.num_units; u += npairs) {
+      int t, part;
+      decode_unit(p, u, t, part);
       int m0, nt, z1, z2;
       decode_tile<TM>(p, t, m0, nt, z1, z2);
       int n0 = nt * BN;
       if (tile_skipped<TM>(p, m0, n0)) continue;
       int kb0, kb1;
-      k_range<TM>(p, m0, kb0, kb1);
+      unit_k_range<TM>(p, m0, part, kb0, kb1);
       const bool have = kb1 > kb0;
+      const bool split = part >= 0;
+      const bool to_ws = split && !p.split_direct;  // partial -> workspace
+      const bool add_r = p.R && !split;              // a split tile's R is added by its finisher
+      const bool f32 = p.c_fp32 || to_ws;
+      const int sidx = t - p.split_first;            // split tile index
+      const int wrow = sidx * TM + BM * int(crank) + ew * 32;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row0 = m0 + BM * int(crank) + ew * 32;  // this warp's 32-row slab
@@ -299,7 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < BN; c += 32) {
           const int col = n0 + c;
           if (col >= p.N) break;
-          if (p.R && lane == 0) {
+          if (add_r && lane == 0) {
             mbar_arrive_expect_tx(&rbar[ew], C::EPI_CHUNK);
             tma_load_4d(rbuf, &tmR, &rbar[ew], col, row0, z1, z2);
           }
@@ -309,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = have ? __uint_as_float(r[i]) * p.alpha : 0.f;
-          if (p.R) {
+          if (add_r) {
             mbar_wait(&rbar[ew], rphase);
             rphase ^= 1;
 #pragma unroll
@@ -325,26 +390,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) bulk_wait_read<1>();
           __syncwarp();
           uint8_t* sbuf = ebuf + sb * C::EPI_CHUNK;
-          if (p.c_fp32) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              *reinterpret_cast<float4*>(sbuf + swz<128>(lane, q)) =
-                  make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-          } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint4 w;
-              w.x = pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
-              w.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
-              w.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
-              w.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
-              *reinterpret_cast<uint4*>(sbuf + swz<64>(lane, q)) = w;
-            }
-          }
+          stage_chunk(sbuf, v, f32, lane);
           fence_async_shared();
           __syncwarp();
           if (lane == 0) {
-            if (p.beta)
+            if (to_ws)
+              tma_reduce_add_4d(&tmW, sbuf, c, wrow, 0, 0);
+            else if (p.beta || split)
               tma_reduce_add_4d(&tmC, sbuf, col, row0, z1, z2);
             else
               tma_store_4d(&tmC, sbuf, col, row0, z1, z2);
@@ -364,6 +416,89 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
+      }
+      if (to_ws && row0 < p.M) {
+        // publish the partial; the last of the split_s partials of this slab
+        // sums the workspace slab into C and leaves slab and counter zero
+        int* cnt = p.ws_cnt + sidx * (4 * CG) + int(crank) * 4 + ew;
+        int old = 0;
+        if (lane == 0) {
+          bulk_wait_all();
+          fence_proxy_async_global();
+          __threadfence();
+          old = atomicAdd(cnt, 1);
+          if (old == p.split_s - 1) {
+            __threadfence();
+            fence_proxy_async_global();
+          }
+        }
+        old = __shfl_sync(0xffffffffu, old, 0);
+        __syncwarp();
+        if (old == p.split_s - 1) {
+          // coalesced reads of the workspace slab (lane -> rows lr + 4j, float4
+          // column lq), two chunks in flight; transposed through rbuf into the
+          // row-per-lane staging layout of the store path
+          const int lr = lane >> 3, lq = lane & 7;
+          float* wbase = p.ws + (long long)wrow * BN + 4 * lq;
+          const int nch = (min(BN, p.N - n0) + 31) / 32;
+          float4 cur[8], nxt[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            cur[j] = __ldcg(reinterpret_cast<const float4*>(wbase + (long long)(lr + 4 * j) * BN));
+#pragma unroll 1
+          for (int ci = 0; ci < nch; ++ci) {
+            const int c = ci * 32;
+            const int col = n0 + c;
+            if (ci + 1 < nch) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                nxt[j] = __ldcg(reinterpret_cast<const float4*>(wbase + (long long)(lr + 4 * j) * BN + c + 32));
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              __stcg(reinterpret_cast<float4*>(wbase + (long long)(lr + 4 * j) * BN + c),
+                     make_float4(0.f, 0.f, 0.f, 0.f));
+            if (p.R && col + 4 * lq < p.N) {
+              const float* rs = p.R + (long long)z1 * p.cbs1 + (long long)z2 * p.cbs2 + col + 4 * lq;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const int row = row0 + lr + 4 * j;
+                if (row < p.M) {
+                  const float4 o = __ldcg(reinterpret_cast<const float4*>(rs + (long long)row * p.ldc));
+                  cur[j].x += o.x; cur[j].y += o.y; cur[j].z += o.z; cur[j].w += o.w;
+                }
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<float4*>(rbuf + swz<128>(lr + 4 * j, lq)) = cur[j];
+            __syncwarp();
+            float v[32];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 o = *reinterpret_cast<const float4*>(rbuf + swz<128>(lane, q));
+              v[4 * q] = o.x; v[4 * q + 1] = o.y; v[4 * q + 2] = o.z; v[4 * q + 3] = o.w;
+            }
+            __syncwarp();
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+            uint8_t* sbuf = ebuf + sb * C::EPI_CHUNK;
+            stage_chunk(sbuf, v, p.c_fp32, lane);
+            fence_async_shared();
+            __syncwarp();
+            if (lane == 0) {
+              if (p.beta)
+                tma_reduce_add_4d(&tmC, sbuf, col, row0, z1, z2);
+              else
+                tma_store_4d(&tmC, sbuf, col, row0, z1, z2);
+              bulk_commit();
+            }
+            sb ^= 1;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) cur[j] = nxt[j];
+          }
+          if (lane == 0) atomicExch(cnt, 0);
+        }
       }
     }
     if (lane == 0) bulk_wait_all();
@@ -450,7 +585,8 @@ bool make_map_c(CUtensorMap* map, void* ptr, int fp32, long long N, long long M,
 
 template <int BN, int AM, int BMn, int CG>
 cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
-                     const CUtensorMap& mr, const EpiParams& p, cudaStream_t s) {
+                     const CUtensorMap& mr, const CUtensorMap& mw, EpiParams p, int grid,
+                     cudaStream_t s) {
   using C = Cfg<BN, CG>;
   static bool attr_done = false;
   auto kern = gemm_kernel<BN, AM, BMn, CG>;
@@ -460,8 +596,6 @@ cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  int sms = g_sm_limit > 0 ? std::min(g_sm_limit, g_num_sms) : g_num_sms;
-  int grid = std::min(p.num_tiles * CG, (sms / CG) * CG);
   if (grid <= 0) return cudaSuccess;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -475,17 +609,42 @@ cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mr, p);
+  return cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mr, mw, p);
 }
 
 template <int BN, int CG>
 cudaError_t dispatch_major(int am, int bm, const CUtensorMap& ma, const CUtensorMap& mb,
-                           const CUtensorMap& mc, const CUtensorMap& mr, const EpiParams& p,
-                           cudaStream_t s) {
-  if (!am && !bm) return launch_t<BN, 0, 0, CG>(ma, mb, mc, mr, p, s);
-  if (!am && bm) return launch_t<BN, 0, 1, CG>(ma, mb, mc, mr, p, s);
-  if (am && !bm) return launch_t<BN, 1, 0, CG>(ma, mb, mc, mr, p, s);
-  return launch_t<BN, 1, 1, CG>(ma, mb, mc, mr, p, s);
+                           const CUtensorMap& mc, const CUtensorMap& mr, const CUtensorMap& mw,
+                           const EpiParams& p, int grid, cudaStream_t s) {
+  if (!am && !bm) return launch_t<BN, 0, 0, CG>(ma, mb, mc, mr, mw, p, grid, s);
+  if (!am && bm) return launch_t<BN, 0, 1, CG>(ma, mb, mc, mr, mw, p, grid, s);
+  if (am && !bm) return launch_t<BN, 1, 0, CG>(ma, mb, mc, mr, mw, p, grid, s);
+  return launch_t<BN, 1, 1, CG>(ma, mb, mc, mr, mw, p, grid, s);
+}
+
+// Split of the tail wave: T tiles on P pairs run q = T / P full rounds and a
+// last round of r = T % P tiles.  Cutting those r tiles into s k-ranges costs
+// ceil(r*s / P) rounds of (1/s + ovh) tile times instead of 1, where ovh is
+// the per-part epilogue price measured on B200 (partial reduce-add; plus the
+// workspace round trip of the finishing part).  Pick the s (<= 8, >= 4
+// k-blocks per part) with the smallest cost; split only if the whole GEMM
+// gets >= 4% faster.  Returns 1 when no split pays.
+int choose_split(int T, int P, int kblocks, bool direct) {
+  const int r = T % P;
+  if (r == 0 || P <= 1) return 1;
+  const double ovh = direct ? 0.08 : 0.35;
+  const int q = T / P;
+  int best = 1;
+  double best_cost = 1.0;
+  for (int s = 2; s <= 8 && kblocks / s >= 4; ++s) {
+    const double cost = double((r * s + P - 1) / P) * (1.0 / s + ovh);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = s;
+    }
+  }
+  if (best > 1 && (q + best_cost) > 0.96 * (q + 1)) best = 1;
+  return best;
 }
 
 }  // namespace
@@ -544,13 +703,41 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream) {
   } else {
     mr = mc;
   }
+  const int sms = g_sm_limit > 0 ? std::min(g_sm_limit, g_num_sms) : g_num_sms;
+  const int P = std::max(1, sms / CG);
+  // tail split (dense GEMMs only)
+  p.split_first = p.num_tiles;
+  p.split_s = 1;
+  p.num_units = p.num_tiles;
+  p.split_direct = 0;
+  p.ws = d.ws;
+  p.ws_cnt = d.ws_cnt;
+  CUtensorMap mw = mc;
+  if (d.causal == kCausalNone && d.split != 0 && p.num_tiles > 0) {
+    const int kblocks = (d.K + BK - 1) / BK;
+    const bool direct = d.beta && !d.R;
+    int s = d.split > 1 ? std::min(d.split, std::max(1, kblocks))
+                        : choose_split(p.num_tiles, P, kblocks, direct);
+    const int r = d.split > 1 ? std::min(p.num_tiles, P) : p.num_tiles % P;
+    const int nsplit = r;
+    const bool ws_ok = d.ws && d.ws_cnt && size_t(nsplit) * TM * BN * 4 <= d.ws_bytes &&
+                       nsplit * 4 * CG <= d.ws_cnt_n &&
+                       make_map_c(&mw, d.ws, 1, BN, (long long)nsplit * TM, BN, 0, 0, 1, 1);
+    if (s > 1 && r > 0 && (direct || ws_ok)) {
+      p.split_first = p.num_tiles - r;
+      p.split_s = s;
+      p.num_units = p.split_first + r * s;
+      p.split_direct = direct ? 1 : 0;
+    }
+  }
+  const int grid = std::min(p.num_units, P) * CG;
   const int am = d.A.mn_major, bmj = d.B.mn_major;
   if (CG == 2) {
-    if (BN == 256) return dispatch_major<256, 2>(am, bmj, ma, mb, mc, mr, p, stream);
-    return dispatch_major<128, 2>(am, bmj, ma, mb, mc, mr, p, stream);
+    if (BN == 256) return dispatch_major<256, 2>(am, bmj, ma, mb, mc, mr, mw, p, grid, stream);
+    return dispatch_major<128, 2>(am, bmj, ma, mb, mc, mr, mw, p, grid, stream);
   }
-  if (BN == 256) return dispatch_major<256, 1>(am, bmj, ma, mb, mc, mr, p, stream);
-  return dispatch_major<128, 1>(am, bmj, ma, mb, mc, mr, p, stream);
+  if (BN == 256) return dispatch_major<256, 1>(am, bmj, ma, mb, mc, mr, mw, p, grid, stream);
+  return dispatch_major<128, 1>(am, bmj, ma, mb, mc, mr, mw, p, grid, stream);
 }
 
 }  // namespace hexexec

@@ -1,7 +1,7 @@
-// Memory-bound kernels of the step (see kernels.h).  All row-wise kernels use
-// one warp per row, 16-byte vector accesses where the row width allows, and
-// warp-shuffle reductions; elementwise kernels are grid-stride with the grid
-// sized to a multiple of the SM count.
+// Memory-bound kernels of the step (see kernels.h): 16-byte vector accesses
+// where the row width allows; RMSNorm as CTA row bands (block reduction per
+// row); elementwise kernels grid-stride with the grid sized to a multiple of
+// the SM count.  Each kernel's HBM bytes and measured GB/s: scripts/bench_ew.py.
 #include <cfloat>
 
 #include "common.cuh"
@@ -191,8 +191,9 @@ __global__ void residual_add_kernel(const float* x, const bf16* y, float* xo, lo
 // 1-D bulk copies (x, dy, dres of one row per stage):
 //   c   = r^3/H * sum_j dy*g*x            (block reduction per row)
 //   dx  = dres + r*dy*g - x*c
-//   dg += sum_rows dy*x*r                 (registers over the CTA's rows,
-//                                          one atomic per column per CTA)
+//   dg += sum_rows dy*x*r                 (registers over the CTA's rows, one
+//                                          partial row per CTA, summed in CTA
+//                                          order by colsum_add_kernel)
 // Stage reuse needs no extra barrier: the per-row reduction barrier of row k
 // proves every thread has finished row k-1, whose stage is refilled then.
 // Thread t owns columns c*2048 + q*1024 + 4t .. +3 (q = 0, 1): conflict-free
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(kNormThreads, NC <= 2 ? 2 : 1)
     rmsnorm_bwd_kernel(const bf16* __restrict__ dyb, const float* __restrict__ dyf,
                        const float* __restrict__ x, const float* __restrict__ rstd,
                        const float* __restrict__ g, const float* dres, float* dx,
-                       bf16* __restrict__ dxb, float* __restrict__ dg, int M, int H, int nst) {
+                       bf16* __restrict__ dxb, float* __restrict__ dg_part, int M, int H, int nst) {
   extern __shared__ uint8_t nsm_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(nsm_raw) + 127) & ~uintptr_t(127));
   __shared__ float red[16];
@@ -324,10 +325,33 @@ __global__ void __launch_bounds__(kNormThreads, NC <= 2 ? 2 : 1)
     for (int q = 0; q < 2; ++q) {
       const int col = c * kNormChunk + q * (kNormChunk / 2) + threadIdx.x * 4;
       if (col < H) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) atomicAdd(dg + col + e, acc[c][4 * q + e]);
+        *reinterpret_cast<float4*>(dg_part + (long long)blockIdx.x * H + col) =
+            make_float4(acc[c][4 * q], acc[c][4 * q + 1], acc[c][4 * q + 2], acc[c][4 * q + 3]);
       }
     }
+}
+
+// dg[j] += sum of the CTA partial rows, in a fixed order (deterministic):
+// block = 32 columns x 8 row groups; group g sums rows g, g+8, ... then the
+// 8 group sums are added in group order
+__global__ void colsum_add_kernel(const float* __restrict__ part, int rows, int H,
+                                  float* __restrict__ dg) {
+  __shared__ float red[8][33];
+  const int j = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int grp = threadIdx.x >> 5;
+  float s = 0.f;
+  if (j < H) {
+#pragma unroll 4
+    for (int r = grp; r < rows; r += 8) s += part[(long long)r * H + j];
+  }
+  red[grp][threadIdx.x & 31] = s;
+  __syncthreads();
+  if (grp == 0 && j < H) {
+    float t = red[0][threadIdx.x];
+#pragma unroll
+    for (int g = 1; g < 8; ++g) t += red[g][threadIdx.x];
+    dg[j] += t;
+  }
 }
 
 // ------------------------------------------------------------------ rope
@@ -687,15 +711,13 @@ void k_residual_add(const float* x, const bf16* y, float* xo, long long n, cudaS
 }
 void k_rmsnorm_bwd(const bf16* dyb, const float* dyf, const float* x, const float* rstd,
                    const float* g, const float* dres, float* dx, bf16* dxb, float* dg, int M,
-                   int H, cudaStream_t s) {
+                   int H, float* dg_part, cudaStream_t s) {
   if (M <= 0) return;
-  // persistent CTAs (two per SM while H <= 4096 so one CTA's row barrier
-  // overlaps the other's copies); each CTA's rows end in one dg atomic per column
+  // one persistent CTA per SM; each CTA's rows end in one partial dg row
   const int nc = (H + kNormChunk - 1) / kNormChunk;
-  const int per_sm = 1;
-  const int grid = std::min(M, kNumSmsHint * per_sm);
+  const int grid = std::min(M, kRmsBwdCtas);
   const size_t stage = size_t(H) * (4 + (dyb ? 2 : 4) + (dres ? 4 : 0));
-  const size_t budget = per_sm == 2 ? (100u << 10) : (200u << 10);
+  const size_t budget = 200u << 10;
   const int nst = int(std::max<size_t>(1, std::min<size_t>(kNormStages, budget / stage)));
   const size_t smem = stage * nst + 128;
 #define HX_NORM_BWD(NC, B)                                                                   \
@@ -707,7 +729,7 @@ void k_rmsnorm_bwd(const bf16* dyb, const float* dyf, const float* x, const floa
       attr = true;                                                                          \
     }                                                                                       \
     rmsnorm_bwd_kernel<NC, B><<<grid, kNormThreads, smem, s>>>(dyb, dyf, x, rstd, g, dres, dx, \
-                                                                dxb, dg, M, H, nst);        \
+                                                                dxb, dg_part, M, H, nst);   \
   } while (0)
 #define HX_NORM_BWD_NC(B)       \
   if (nc <= 1) HX_NORM_BWD(1, B); \
@@ -721,6 +743,7 @@ void k_rmsnorm_bwd(const bf16* dyb, const float* dyf, const float* x, const floa
   }
 #undef HX_NORM_BWD_NC
 #undef HX_NORM_BWD
+  colsum_add_kernel<<<(H + 31) / 32, 256, 0, s>>>(dg_part, grid, H, dg);
 }
 void k_rope(bf16* qkv, int M, int S, int nh, int d, float theta, int inverse, cudaStream_t s) {
   long long n = (long long)M * ((nh + kRopeHeads - 1) / kRopeHeads) * (d / 16);

@@ -1,7 +1,8 @@
 // Memory-bound kernels of the training step (sm_100a): init, tokens,
 // embedding, RMSNorm, RoPE, causal softmax, SwiGLU, vocab-parallel cross
-// entropy, DP gradient scale+cast, AdamW.  Row-wise ops use one warp per row
-// with 16-byte vector accesses and warp-shuffle reductions.
+// entropy, DP gradient scale+cast, AdamW.  RMSNorm runs row bands per CTA
+// (the backward through a bulk-copy shared-memory ring); the other row-wise
+// ops use a warp or CTA per row; all with 16-byte vector accesses.
 #pragma once
 
 #include <cuda_bf16.h>
@@ -73,10 +74,12 @@ void k_residual_add(const float* x, const bf16* y, float* xo, long long n, cudaS
 // dx = dres + rmsnorm_bwd(dy);  dx_bf16 optional copy;  dg += sum_m dy*xhat
 // dy is bf16 if dy_bf16 != null else fp32 (dy_f32)
 // Safe in place (dx == dres): each element is read then written by the same
-// thread.
+// thread.  dg_part: fp32 scratch of kRmsBwdCtas * H (per-CTA partial dg rows,
+// summed in a fixed order so dg is bitwise reproducible).
+constexpr int kRmsBwdCtas = 148;
 void k_rmsnorm_bwd(const bf16* dy_bf16, const float* dy_f32, const float* x, const float* rstd,
                    const float* g, const float* dres, float* dx, bf16* dx_bf16, float* dg, int M,
-                   int H, cudaStream_t s);
+                   int H, float* dg_part, cudaStream_t s);
 
 // in-place rotary embedding of q and k inside the fused [M, nh*3*d] buffer
 // (rotate-half convention); inverse=1 applies the transpose (backward).

@@ -13,6 +13,19 @@ from paper_2409_01143_b200 import _lib as L  # noqa: E402
 PEAK = 1661.7
 
 
+WS = None
+
+
+def set_split(mode):
+    """mode: -1 auto tail split (with workspace), 0 off"""
+    global WS
+    if WS is None:
+        WS = (torch.zeros(148 * 128 * 256, device="cuda"),
+              torch.zeros(148 * 8, device="cuda", dtype=torch.int32))
+    assert L.hexexec_k_gemm_split(mode, WS[0].data_ptr(), WS[0].numel() * 4, WS[1].data_ptr(),
+                                  WS[1].numel()) == 0
+
+
 def run(M, N, K, a_mn=0, b_mn=0, c32=0, beta=0, iters=10, tag=""):
     A = (torch.randn(K, M) if a_mn else torch.randn(M, K)).cuda().bfloat16()
     B = (torch.randn(K, N) if b_mn else torch.randn(N, K)).cuda().bfloat16()
@@ -45,6 +58,10 @@ def run(M, N, K, a_mn=0, b_mn=0, c32=0, beta=0, iters=10, tag=""):
 
 CASES = [
     ("qkv fwd", 2048, 12288, 4096, 0, 0, 0, 0),
+    ("o fwd bf16", 2048, 4096, 4096, 0, 1, 0, 0),
+    ("o wgrad beta", 4096, 4096, 2048, 1, 1, 1, 1),
+    ("o wgrad nobeta", 4096, 4096, 2048, 1, 1, 1, 0),
+    ("qkv wgrad beta", 12288, 4096, 2048, 1, 1, 1, 1),
     ("o fwd fp32", 2048, 4096, 4096, 0, 1, 1, 0),
     ("gu fwd", 2048, 22016, 4096, 0, 0, 0, 0),
     ("down fwd fp32", 2048, 4096, 11008, 0, 1, 1, 0),
@@ -62,4 +79,10 @@ if __name__ == "__main__":
     sel = sys.argv[1:]
     for c in CASES:
         if not sel or any(s in c[0] for s in sel):
-            print(json.dumps(run(*c[1:], tag=c[0])), flush=True)
+            row = {}
+            for mode, name in ((0, "nosplit"), (-1, "split")):
+                set_split(mode)
+                r = run(*c[1:], tag=c[0])
+                row[name] = r["tflops"]
+            r.update(row)
+            print(json.dumps(r), flush=True)

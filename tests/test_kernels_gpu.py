@@ -41,6 +41,41 @@ def _rel(out, ref):
     return (out.float() - ref.float()).abs().max().item() / max(ref.float().abs().max().item(), 1e-30)
 
 
+@pytest.mark.parametrize("split", [-1, 2, 3, 5])
+@pytest.mark.parametrize("M,N,K,a_mn,b_mn", [(2048, 4096, 1024, 0, 1), (512, 1024, 512, 1, 1),
+                                             (384, 704, 640, 0, 0)])
+def test_gemm_tail_split(cuda, split, M, N, K, a_mn, b_mn):
+    """Split-K of the partial last wave: bf16 / fp32 stores go through the
+    fp32 workspace (last partial finishes the tile), beta GEMMs reduce-add
+    partials into C; workspace and counters must be left zero."""
+    L = _L()
+    ws = torch.zeros(148 * 128 * 256, device=cuda)
+    cnt = torch.zeros(148 * 8, device=cuda, dtype=torch.int32)
+    assert L.hexexec_k_gemm_split(split, ws.data_ptr(), ws.numel() * 4, cnt.data_ptr(),
+                                  cnt.numel()) == 0
+    try:
+        g = torch.Generator(device="cuda").manual_seed(M + N + K)
+        A = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+        B = torch.randn(N, K, device=cuda, generator=g).bfloat16()
+        ref = A.float() @ B.float().T
+        As = A.T.contiguous() if a_mn else A
+        Bs = B.T.contiguous() if b_mn else B
+        for _ in range(2):  # second call checks the workspace was left clean
+            C16 = torch.zeros(M, N, device=cuda, dtype=torch.bfloat16)
+            _gemm(As, a_mn, Bs, b_mn, M, N, K, C16)
+            assert _rel(C16, ref) < 1e-2
+            C32 = torch.zeros(M, N, device=cuda)
+            _gemm(As, a_mn, Bs, b_mn, M, N, K, C32, alpha=0.5)
+            assert _rel(C32, 0.5 * ref) < 2e-3
+            acc = torch.ones(M, N, device=cuda)
+            _gemm(As, a_mn, Bs, b_mn, M, N, K, acc, beta=1)
+            assert _rel(acc, ref + 1) < 2e-3
+        assert ws.abs().max().item() == 0.0
+        assert cnt.abs().max().item() == 0
+    finally:
+        L.hexexec_k_gemm_split(-1, None, 0, None, 0)
+
+
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
 @pytest.mark.parametrize("M,N,K", [(256, 512, 256), (384, 192, 192), (128, 2752, 128),
                                    (304, 200, 96)])
