@@ -297,6 +297,49 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// Softmax row pieces, specialised on the diagonal tile so the causal mask
+// costs nothing on the other tiles (one thread = one row r of the tile).
+template <bool DIAG>
+HX_DEVICE float row_max(const uint32_t (&sv)[T], int r) {
+  float mx[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) mx[k] = -FLT_MAX;
+#pragma unroll
+  for (int i = 0; i < T; ++i) {
+    const float v = __uint_as_float(sv[i]);
+    mx[i % 8] = (!DIAG || i <= r) ? fmaxf(mx[i % 8], v) : mx[i % 8];
+  }
+  return fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+               fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+}
+
+// P = exp2(s * scale_log2 - m) -> bf16 K-major smem rows; returns the row sum
+template <bool DIAG>
+HX_DEVICE float exp_store_p(const uint32_t (&sv)[T], int r, float scale_log2, float m,
+                            uint8_t* myP) {
+  float lsp[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) lsp[k] = 0.f;
+#pragma unroll
+  for (int q = 0; q < T / 8; ++q) {
+    float pv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = q * 8 + k;
+      const float e = ex2(fmaf(__uint_as_float(sv[i]), scale_log2, -m));
+      pv[k] = (!DIAG || i <= r) ? e : 0.f;
+      lsp[k] += pv[k];
+    }
+    uint4 w;
+    w.x = pack_bf16x2(pv[0], pv[1]);
+    w.y = pack_bf16x2(pv[2], pv[3]);
+    w.z = pack_bf16x2(pv[4], pv[5]);
+    w.w = pack_bf16x2(pv[6], pv[7]);
+    *reinterpret_cast<uint4*>(myP + kchunk(r, q)) = w;
+  }
+  return ((lsp[0] + lsp[1]) + (lsp[2] + lsp[3])) + ((lsp[4] + lsp[5]) + (lsp[6] + lsp[7]));
+}
+
 // ------------------------------------------------------------------ forward, 2 Q tiles
 // CTA = one (sample, head) and the query-tile pair (2t, 2t+1).  Two softmax
 // warpgroups (A: warps 4-7, B: warps 8-11) ping-pong: while one computes its
@@ -423,6 +466,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
                      id_o, (j > 0 || ks > 0) ? 1u : 0u);
         tc_commit(&o_full[g]);
       };
+      // S_g(j+1) is issued as soon as warpgroup g has read S_g(j) out of TMEM,
+      // so it computes during the softmax of tile j and both warpgroups'
+      // softmax run concurrently (latency hiding across the pair)
       if (nt_a > 0) issue_s(0, 0);
       if (has_b) issue_s(1, 0);
       for (int j = 0; j < nkv; ++j) {
@@ -477,15 +523,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[g]);
-        float mx[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) mx[k] = -FLT_MAX;
-#pragma unroll
-        for (int i = 0; i < T; ++i)
-          if (!diag || i <= r) mx[i % 8] = fmaxf(mx[i % 8], __uint_as_float(sv[i]));
-        float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                         fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-        mt *= p.scale_log2;
+        float mt = (diag ? row_max<true>(sv, r) : row_max<false>(sv, r)) * p.scale_log2;
         if (j > 0) {  // PV_{j-1} done: P buffer free and O stable
           mbar_wait(&o_full[g], (j - 1) & 1);
           tc_fence_after();
@@ -508,27 +546,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
           l *= alpha;
           m = m_new;
         }
-        float lsp[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) lsp[k] = 0.f;
-#pragma unroll
-        for (int q = 0; q < T / 8; ++q) {
-          float pv[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int i = q * 8 + k;
-            const float e = ex2(fmaf(__uint_as_float(sv[i]), p.scale_log2, -m));
-            pv[k] = (!diag || i <= r) ? e : 0.f;
-            lsp[k] += pv[k];
-          }
-          uint4 w;
-          w.x = pack_bf16x2(pv[0], pv[1]);
-          w.y = pack_bf16x2(pv[2], pv[3]);
-          w.z = pack_bf16x2(pv[4], pv[5]);
-          w.w = pack_bf16x2(pv[6], pv[7]);
-          *reinterpret_cast<uint4*>(myP + kchunk(r, q)) = w;
-        }
-        l += ((lsp[0] + lsp[1]) + (lsp[2] + lsp[3])) + ((lsp[4] + lsp[5]) + (lsp[6] + lsp[7]));
+        l += diag ? exp_store_p<true>(sv, r, p.scale_log2, m, myP)
+                  : exp_store_p<false>(sv, r, p.scale_log2, m, myP);
         tc_fence_before();
         fence_async_shared();
         __syncwarp();
@@ -590,6 +609,33 @@ struct BwdCfg {
   static constexpr uint32_t PDS = T * T * 2;
   static constexpr uint32_t SMEM = 1024 + 6 * TILE + PDS + 2 * T * 4 + 256;
 };
+
+// P^T row kr of a query tile: pk (S^T in, P^T out, kept for the dS pass) and
+// the bf16 copy for the dV product; the causal mask only on the diagonal tile
+template <bool DIAG>
+HX_DEVICE void bwd_p_tile(float (&pk)[T], const float* sLse, float scale_log2, int kr,
+                          uint8_t* sPD) {
+#pragma unroll
+  for (int q8 = 0; q8 < T / 8; ++q8) {
+    const float4 la = *reinterpret_cast<const float4*>(sLse + q8 * 8);
+    const float4 lb = *reinterpret_cast<const float4*>(sLse + q8 * 8 + 4);
+    const float ls[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
+    float pr[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int qc = q8 * 8 + k;
+      const float e = ex2(fmaf(pk[qc], scale_log2, -ls[k]));
+      pr[k] = (DIAG && kr > qc) ? 0.f : e;
+      pk[qc] = pr[k];
+    }
+    uint4 w;
+    w.x = pack_bf16x2(pr[0], pr[1]);
+    w.y = pack_bf16x2(pr[2], pr[3]);
+    w.z = pack_bf16x2(pr[4], pr[5]);
+    w.w = pack_bf16x2(pr[6], pr[7]);
+    *reinterpret_cast<uint4*>(sPD + kchunk(kr, q8)) = w;
+  }
+}
 
 template <int NATOMS_UNUSED>
 HX_DEVICE uint64_t mnview(uint32_t base, int ks) {
@@ -784,26 +830,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(s_read);  // S region may take S_{t+1} now
-#pragma unroll
-      for (int q8 = 0; q8 < T / 8; ++q8) {
-        const float4 la = *reinterpret_cast<const float4*>(sLse + q8 * 8);
-        const float4 lb = *reinterpret_cast<const float4*>(sLse + q8 * 8 + 4);
-        const float ls[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
-        float pr[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int qc = q8 * 8 + k;
-          const float e = ex2(fmaf(pk[qc], p.scale_log2, -ls[k]));
-          pr[k] = (diag && kr > qc) ? 0.f : e;
-          pk[qc] = pr[k];
-        }
-        uint4 w;
-        w.x = pack_bf16x2(pr[0], pr[1]);
-        w.y = pack_bf16x2(pr[2], pr[3]);
-        w.z = pack_bf16x2(pr[4], pr[5]);
-        w.w = pack_bf16x2(pr[6], pr[7]);
-        *reinterpret_cast<uint4*>(sPD + kchunk(kr, q8)) = w;
-      }
+      if (diag)
+        bwd_p_tile<true>(pk, sLse, p.scale_log2, kr, sPD);
+      else
+        bwd_p_tile<false>(pk, sLse, p.scale_log2, kr, sPD);
       fence_async_shared();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
