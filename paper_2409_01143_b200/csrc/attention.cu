@@ -92,8 +92,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const int nqt = p.S / T;
-  const int qt = nqt - 1 - int(blockIdx.x % nqt);  // heaviest query tiles first
-  const int zh = int(blockIdx.x / nqt);
+  // heaviest query tiles of every head first (longest-first over the grid)
+  const int nz = p.mb * p.nh;
+  const int qt = nqt - 1 - int(blockIdx.x / nz);
+  const int zh = int(blockIdx.x % nz);
   const int h = zh % p.nh;
   const int b = zh / p.nh;
   const int ntiles = qt + 1;
@@ -385,8 +387,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
   const int lane = threadIdx.x % 32;
   const int nqt = p.S / T;
   const int npairs = (nqt + 1) / 2;
-  const int pr = npairs - 1 - int(blockIdx.x % npairs);  // heaviest pairs first
-  const int zh = int(blockIdx.x / npairs);
+  // heaviest pairs of every head first (longest-first over the grid)
+  const int nz = p.mb * p.nh;
+  const int pr = npairs - 1 - int(blockIdx.x / nz);
+  const int zh = int(blockIdx.x % nz);
   const int h = zh % p.nh;
   const int b = zh / p.nh;
   const int qa = 2 * pr;                 // query tile of warpgroup A
@@ -677,8 +681,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const int nt = p.S / T;
-  const int kt = int(blockIdx.x % nt);  // small kt = most query tiles: launched first
-  const int zh = int(blockIdx.x / nt);
+  // small kt = most query tiles: every head's kt = 0 first (longest-first)
+  const int nz = p.mb * p.nh;
+  const int kt = int(blockIdx.x / nz);
+  const int zh = int(blockIdx.x % nz);
   const int h = zh % p.nh;
   const int b = zh / p.nh;
   const int ntiles = nt - kt;
