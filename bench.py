@@ -140,6 +140,9 @@ def gather_sum(vals: list, rank: int, world: int, tag: str) -> list:
     return [sum(v[i] for v in allv) for i in range(len(vals))]
 
 
+EXEC_CFG = {}  # --exec-config: extra executor config keys (e.g. {"recompute": true})
+
+
 def log(rank: int, msg: str):
     print(f"[bench rank {rank} {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
 
@@ -148,7 +151,7 @@ def run_plan(name: str, steps: int, warmup: int, rank: int, world: int, clocks: 
     from paper_2409_01143_b200 import dist
     c, m, p, idx = load(name)
     log(rank, f"{name}: creating executor")
-    ex = dist.make_executor(c, m, p, {}, tag=f"uid-{name}")
+    ex = dist.make_executor(c, m, p, dict(EXEC_CFG), tag=f"uid-{name}")
     role = ex.role
     # ---- profiled pass first (eager, CUDA events around every GEMM and after every
     # op): roofline evidence for the TP GEMMs + per-kernel-class step timeline.
@@ -290,7 +293,9 @@ def main():
     ap.add_argument("--even", default=None, help="even-split comparison plan ('none' to skip)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exec-config", default="{}", help="JSON executor config overrides")
     a = ap.parse_args()
+    EXEC_CFG.update(json.loads(a.exec_config))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world != a.gpus and "RANK" in os.environ:
@@ -310,6 +315,8 @@ def main():
               "seq_len": model["seq_len"], "even_split_plan": even,
               "l2": "working set per step >> 126 MB L2 (weights + optimizer state + activations)",
               "parallelism": "plan-defined asymmetric DP/PP/TP, one process per GPU"}
+    if EXEC_CFG:
+        config["exec_config"] = dict(EXEC_CFG)
 
     if a.impl == "reference":
         if rank != 0:

@@ -74,6 +74,7 @@ ExecConfig parse_exec_config(const std::string& text) {
       else if (k == "attention") c.attention = v.get<std::string>();
       else if (k == "dp_overlap") c.dp_overlap = v.get<bool>();
       else if (k == "gemm_split") c.gemm_split = v.get<bool>();
+      else if (k == "recompute") c.recompute = v.get<bool>();
       else throw ParseError("exec config: unknown key '" + k + "'");
     } catch (const nlohmann::json::exception& e) {
       throw ParseError("exec config: bad value for '" + k + "'");
@@ -197,6 +198,7 @@ class Executor {
   float* gemm_ws_ = nullptr;  // zero between GEMMs (the kernel leaves it zero)
   int* gemm_cnt_ = nullptr;
   float* dg_part_ = nullptr;
+  LayerActs rc_acts_{};  // recompute: the one shared activation set
   int32_t* tokens = nullptr;
   int32_t* tokens_pinned = nullptr;
   float* idle_loss_ = nullptr;
@@ -423,19 +425,23 @@ class Executor {
     arena.reserve(P * 4 * 4);            // P32, G32, M, V
     arena.reserve(P * 2);                // P16
     if (need_g16) arena.reserve(P * 2);  // DP comm buffer
-    // activations per slot
+    // activations per slot (with recompute: layer inputs only, plus one
+    // shared set of layer activations)
+    const int64_t act_sets = cfg.recompute ? 0 : nl;
+    auto reserve_acts = [&] {
+      arena.reserve(M * H * 4);                  // x_mid
+      arena.reserve(M * H * 2 * 2);              // xn, hn
+      arena.reserve(M * 4 * 2);                  // rstd1, rstd2
+      arena.reserve(M * qkvw * 2);               // qkv
+      arena.reserve(SS * 2);                     // P (unfused)
+      arena.reserve(LSE * 4);                    // lse (fused)
+      arena.reserve(M * kr * 2);                 // attn
+      arena.reserve(M * 2 * F * 2 + M * F * 2);  // gu, act
+    };
+    if (cfg.recompute) reserve_acts();
     for (int s = 0; s < n_slots; ++s) {
       for (int64_t l = 0; l <= nl; ++l) arena.reserve(M * H * 4);
-      for (int64_t l = 0; l < nl; ++l) {
-        arena.reserve(M * H * 4);                  // x_mid
-        arena.reserve(M * H * 2 * 2);              // xn, hn
-        arena.reserve(M * 4 * 2);                  // rstd1, rstd2
-        arena.reserve(M * qkvw * 2);               // qkv
-        arena.reserve(SS * 2);                     // P (unfused)
-        arena.reserve(LSE * 4);                    // lse (fused)
-        arena.reserve(M * kr * 2);                 // attn
-        arena.reserve(M * 2 * F * 2 + M * F * 2);  // gu, act
-      }
+      for (int64_t l = 0; l < act_sets; ++l) reserve_acts();
       if (role.last_stage) {
         arena.reserve(M * H * 2 + M * 4);
         arena.reserve(M * Vr * 2);
@@ -454,6 +460,13 @@ class Executor {
     arena.reserve(kGemmWsCounters * 4);
     arena.reserve(size_t(kRmsBwdCtas) * H * 4);             // rmsnorm bwd partial dg rows
     arena.reserve(role.batch * (S + 1) * 4);               // tokens
+    // memory tier: the device's memory_gib caps the rank (cost_model.cpp:130-153
+    // applies the same per-device budget to its layer-memory estimate)
+    const double cap = L.cluster.devices[size_t(role.device)].memory_gib * double(1ull << 30);
+    if (double(arena.total()) > cap)
+      throw Infeasible("plan does not fit device '" + L.cluster.devices[size_t(role.device)].id +
+                       "': rank needs " + std::to_string(arena.total() >> 20) + " MiB, memory_gib " +
+                       std::to_string(L.cluster.devices[size_t(role.device)].memory_gib));
     if (cfg.validate_only) return;
     arena.commit();
 
@@ -463,24 +476,26 @@ class Executor {
     Vo = arena.take<float>(P);
     P16 = arena.take<bf16>(P);
     if (need_g16) G16 = arena.take<bf16>(P);
+    auto take_acts = [&] {
+      LayerActs a;
+      a.x_mid = arena.take<float>(M * H);
+      a.xn = arena.take<bf16>(M * H);
+      a.hn = arena.take<bf16>(M * H);
+      a.rstd1 = arena.take<float>(M);
+      a.rstd2 = arena.take<float>(M);
+      a.qkv = arena.take<bf16>(M * qkvw);
+      a.P = arena.take<bf16>(SS);
+      a.lse = arena.take<float>(LSE);
+      a.attn = arena.take<bf16>(M * kr);
+      a.gu = arena.take<bf16>(M * 2 * F);
+      a.act = arena.take<bf16>(M * F);
+      return a;
+    };
+    if (cfg.recompute) rc_acts_ = take_acts();
     slots.resize(size_t(n_slots));
     for (auto& sl : slots) {
       for (int64_t l = 0; l <= nl; ++l) sl.x.push_back(arena.take<float>(M * H));
-      for (int64_t l = 0; l < nl; ++l) {
-        LayerActs a;
-        a.x_mid = arena.take<float>(M * H);
-        a.xn = arena.take<bf16>(M * H);
-        a.hn = arena.take<bf16>(M * H);
-        a.rstd1 = arena.take<float>(M);
-        a.rstd2 = arena.take<float>(M);
-        a.qkv = arena.take<bf16>(M * qkvw);
-        a.P = arena.take<bf16>(SS);
-        a.lse = arena.take<float>(LSE);
-        a.attn = arena.take<bf16>(M * kr);
-        a.gu = arena.take<bf16>(M * 2 * F);
-        a.act = arena.take<bf16>(M * F);
-        sl.layers.push_back(a);
-      }
+      for (int64_t l = 0; l < act_sets; ++l) sl.layers.push_back(take_acts());
       if (role.last_stage) {
         sl.xf = arena.take<bf16>(M * H);
         sl.rstdf = arena.take<float>(M);
@@ -704,8 +719,12 @@ class Executor {
   int32_t* tok_of(int64_t mbi) { return tokens + mbi * mb * (S + 1); }
 
   // ------------------------------------------------------------ forward
-  void layer_fwd(Slot& sl, int64_t l) {
-    LayerActs& a = sl.layers[size_t(l)];
+  LayerActs& acts(Slot& sl, int64_t l) { return cfg.recompute ? rc_acts_ : sl.layers[size_t(l)]; }
+
+  // recompute = true: re-run for the backward; the layer output (down
+  // projection and its TP reduction) is not needed and is skipped
+  void layer_fwd(Slot& sl, int64_t l, bool recompute = false) {
+    LayerActs& a = acts(sl, l);
     const LayerW& w = lw[size_t(l)];
     float* x_in = sl.x[size_t(l)];
     float* x_out = sl.x[size_t(l + 1)];
@@ -733,6 +752,7 @@ class Executor {
     gemm(g2(M, 2 * F, H, a.hn, 0, H, w.wgu.p16, 0, H, a.gu, 2 * F, 0));
     k_swiglu_fwd(a.gu, a.act, int(M), int(F), stream);
     kcheck("swiglu_fwd");
+    if (recompute) return;
     if (role.tp == 1) {
       GemmDesc g = g2(M, H, F, a.act, 0, F, w.wdown.p16, 1, H, x_out, H, 1);
       g.R = a.x_mid;
@@ -840,7 +860,8 @@ class Executor {
   // ------------------------------------------------------------ backward
   // dxo: fp32 grad of the layer output (+ bf16 copy dxob); writes dx_in/dxb_in
   void layer_bwd(Slot& sl, int64_t l, const float* dxo, const bf16* dxob, float* dxi, bf16* dxib) {
-    LayerActs& a = sl.layers[size_t(l)];
+    if (cfg.recompute) layer_fwd(sl, l, true);
+    LayerActs& a = acts(sl, l);
     const LayerW& w = lw[size_t(l)];
     const bool first_mb = accum_first_;
     // MLP: down projection

@@ -25,6 +25,10 @@ struct ExecConfig {
   // ~1% of the step); partial sums land in arbitrary order, so it costs
   // run-to-run bitwise determinism and is opt-in
   bool gemm_split = false;
+  // activation recompute: keep only each layer's input per
+  // micro-batch slot and re-run the layer forward (minus its output GEMM)
+  // before the layer backward, into one shared activation set
+  bool recompute = false;
 };
 
 ExecConfig parse_exec_config(const std::string& text);

@@ -41,6 +41,7 @@ def run_plan(name, tmp_path, steps=1, xcfg=None, host_tokens=True, timeout=600):
     world = len(json.load(open(os.path.join(CFG, "clusters", e["cluster"] + ".json")))["devices"])
     if ngpu() < world:
         pytest.skip(f"{name} needs {world} GPUs")
+    os.makedirs(tmp_path, exist_ok=True)
     port = free_port()
     procs = []
     for r in range(world):
@@ -122,3 +123,18 @@ def test_tiny_mixed_four_ranks(tmp_path):
 def test_tiny_three_stage_pipeline_four_ranks(tmp_path):
     # 3-stage 1F1B, TP=2 (widths 1:3) in the middle stage, TP degree changes at both hops
     check_against_oracle("tiny_pp3_4", run_plan("tiny_pp3_4", tmp_path))
+
+
+@pytest.mark.parametrize("name", ["tiny_1", "tiny_pp31", "tiny_tp31"])
+def test_recompute_matches_stored_activations(tmp_path, name):
+    """Activation recompute re-runs each layer forward before
+    its backward; the step must match the stored-activation step and the
+    oracle."""
+    base = run_plan(name, tmp_path / "base", steps=2)
+    rc = run_plan(name, tmp_path / "rc", steps=2, xcfg={"recompute": True})
+    check_against_oracle(name, rc)
+    for a, b in zip(base, rc):
+        assert np.allclose(a["losses"], b["losses"], rtol=1e-6, atol=0)
+        for key in a:
+            if key.endswith("|w"):
+                assert np.allclose(a[key], b[key], rtol=1e-6, atol=1e-7), key

@@ -29,3 +29,36 @@ def test_every_rank_fits(name):
         worst = max(worst, st["arena_bytes"])
         ex.close()
     assert worst + HEADROOM <= B200_BYTES, (name, worst / 2**30)
+
+
+def _dry(c, m, p, cfg, world):
+    from paper_2409_01143_b200.hexexec import Executor
+    worst = 0
+    for r in range(world):
+        ex = Executor(c, m, p, dict(cfg, validate_only=True), rank=r, world_size=world)
+        worst = max(worst, ex.stats()["arena_bytes"])
+        ex.close()
+    return worst
+
+
+def test_recompute_shrinks_activation_memory_and_memory_gib_caps():
+    """Activation recompute keeps only layer inputs per 1F1B slot; the device's
+    memory_gib (cost_model.cpp:130-153 mem_check) caps each rank's arena, so a
+    memory tier that cannot hold stored activations runs with recompute."""
+    from paper_2409_01143_b200.hexexec import HexexecError
+    name = "llama13b_pp3_asymtp"
+    e = INDEX[name]
+    c = json.load(open(os.path.join(CFG, "clusters", e["cluster"] + ".json")))
+    m = open(os.path.join(CFG, "models", e["model"] + ".json")).read()
+    p = open(os.path.join(CFG, "plans", name + ".json")).read()
+    world = len(c["devices"])
+    full = _dry(json.dumps(c), m, p, {}, world)
+    rc = _dry(json.dumps(c), m, p, {"recompute": True}, world)
+    assert rc < 0.9 * full, (rc / 2**30, full / 2**30)
+    cap_gib = (rc + full) / 2 / 2**30
+    for d in c["devices"]:
+        d["memory_gib"] = cap_gib
+    with pytest.raises(HexexecError) as ei:
+        _dry(json.dumps(c), m, p, {}, world)
+    assert "memory_gib" in str(ei.value)
+    assert _dry(json.dumps(c), m, p, {"recompute": True}, world) == rc
