@@ -54,6 +54,17 @@ char* hexexec_plan_serialize(const hexexec_plan* p);
  * dp_groups, TP/PP peers, and the chunk-matched DP segment table. */
 char* hexexec_plan_layout_json(const hexexec_plan* p);
 int hexexec_plan_world_size(const hexexec_plan* p);
+/* The reference cost model on this plan (cost_model.cpp:210-258
+ * iteration_time, report.cpp:66-93 JSON fields), malloc'd into *report_json.
+ * extension = 0: the reference formula (mixed-speed TP stages -> INVALID
+ * "mixed-type tensor parallel stage", like the reference); extension = 1:
+ * TP stage compute = max_r(w_r/sum(w) * FLOPs / c_r) for uneven tp_widths /
+ * mixed device speeds.  Replaces pricing through hexplan's C++ API. */
+hexexec_status hexexec_plan_cost(const hexexec_plan* p, double state_multiplier, int extension,
+                                 char** report_json, char* err, size_t err_len);
+/* MFU in the reference convention (cost_model.cpp:260-265) for a measured
+ * step time over this plan's cluster; 0 for a non-positive time. */
+double hexexec_plan_mfu(const hexexec_plan* p, double seconds);
 void hexexec_plan_free(hexexec_plan* p);
 
 /* ---- NCCL bootstrap ------------------------------------------------------

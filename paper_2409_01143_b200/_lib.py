@@ -44,6 +44,8 @@ hexexec_plan_parse = _sig("hexexec_plan_parse", _st, _c, _c, _c, C.POINTER(_vp),
 hexexec_plan_serialize = _sig("hexexec_plan_serialize", _vp, _vp)
 hexexec_plan_layout_json = _sig("hexexec_plan_layout_json", _vp, _vp)
 hexexec_plan_world_size = _sig("hexexec_plan_world_size", _i, _vp)
+hexexec_plan_cost = _sig("hexexec_plan_cost", _st, _vp, C.c_double, _i, C.POINTER(_vp), _c, _sz)
+hexexec_plan_mfu = _sig("hexexec_plan_mfu", C.c_double, _vp, C.c_double)
 hexexec_plan_free = _sig("hexexec_plan_free", None, _vp)
 # nccl
 hexexec_unique_id_size = _sig("hexexec_unique_id_size", _sz)
@@ -90,7 +92,7 @@ hexexec_string_free = _sig("hexexec_string_free", None, _vp)
 
 EXPORTED = [
     "hexexec_plan_parse", "hexexec_plan_serialize", "hexexec_plan_layout_json",
-    "hexexec_plan_world_size", "hexexec_plan_free", "hexexec_unique_id_size",
+    "hexexec_plan_world_size", "hexexec_plan_cost", "hexexec_plan_mfu", "hexexec_plan_free", "hexexec_unique_id_size",
     "hexexec_unique_id", "hexexec_ctx_create", "hexexec_ctx_free", "hexexec_step",
     "hexexec_step_async", "hexexec_sync", "hexexec_last_loss", "hexexec_timer",
     "hexexec_set_profile",

@@ -13,6 +13,7 @@
 #include <string>
 
 #include "attention.h"
+#include "costmodel.hpp"
 #include "executor.hpp"
 #include "gemm.h"
 #include "kernels.h"
@@ -116,6 +117,31 @@ char* hexexec_plan_layout_json(const hexexec_plan* p) {
 }
 
 int hexexec_plan_world_size(const hexexec_plan* p) { return p ? p->layout.world_size : 0; }
+
+hexexec_status hexexec_plan_cost(const hexexec_plan* p, double state_multiplier, int extension,
+                                 char** report_json, char* err, size_t err_len) {
+  if (!p || !report_json) {
+    set_err(err, err_len, "null argument");
+    return HEXEXEC_ERR_INVALID;
+  }
+  return guarded(err, err_len, [&] {
+    const hexexec::CostReport r = hexexec::iteration_time(
+        p->layout.plan, p->layout.model, p->layout.cluster, state_multiplier, extension != 0);
+    char* s = dup_string(hexexec::serialize_report(r, p->layout.cluster));
+    if (!s) throw std::bad_alloc();
+    *report_json = s;
+  });
+}
+
+double hexexec_plan_mfu(const hexexec_plan* p, double seconds) {
+  if (!p) return 0.0;
+  try {
+    return hexexec::model_flops_utilization(seconds, p->layout.plan.global_batch, p->layout.model,
+                                            p->layout.cluster);
+  } catch (...) {
+    return 0.0;
+  }
+}
 
 void hexexec_plan_free(hexexec_plan* p) { delete p; }
 

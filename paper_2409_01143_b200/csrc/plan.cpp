@@ -96,11 +96,11 @@ Cluster parse_cluster_doc(const std::string& text) {
   ojson j = parse_text(text, "cluster");
   if (!j.contains("machines") || !j["machines"].is_object())
     throw ParseError("cluster: missing 'machines' object");
-  std::set<std::string> machines;
+  std::map<std::string, std::pair<double, double>> machines;  // name -> (bw, lat)
   for (auto& [name, mj] : j["machines"].items()) {
-    positive(mj, "intra_bandwidth_gbps", "machine");
-    nonneg(mj, "intra_latency_us", "machine");
-    machines.insert(name);
+    const double bw = positive(mj, "intra_bandwidth_gbps", "machine") * 1e9;
+    const double lat = nonneg(mj, "intra_latency_us", "machine") * 1e-6;
+    machines[name] = {bw, lat};
   }
   if (!j.contains("devices") || !j["devices"].is_array() || j["devices"].empty())
     throw ParseError("cluster: missing or empty 'devices' array");
@@ -129,8 +129,47 @@ Cluster parse_cluster_doc(const std::string& text) {
   }
   if (!j.contains("inter") || !j["inter"].is_object())
     throw ParseError("cluster: missing 'inter' object");
-  positive(j["inter"], "bandwidth_gbps", "inter");
-  nonneg(j["inter"], "latency_us", "inter");
+  const double inter_bw = positive(j["inter"], "bandwidth_gbps", "inter") * 1e9;
+  const double inter_lat = nonneg(j["inter"], "latency_us", "inter") * 1e-6;
+  // per-pair overrides (json_io.cpp:120-147): unordered pairs, asymmetric
+  // duplicates rejected with the reference's messages
+  std::map<std::pair<int, int>, std::pair<double, double>> ov;
+  if (j.contains("overrides")) {
+    if (!j["overrides"].is_array()) throw ParseError("cluster: 'overrides' must be an array");
+    for (const auto& oj : j["overrides"]) {
+      if (!oj.contains("a") || !oj.contains("b") || !oj["a"].is_string() || !oj["b"].is_string())
+        throw ParseError("override: needs string fields 'a' and 'b'");
+      const std::string a = oj["a"].get<std::string>(), b = oj["b"].get<std::string>();
+      const int ia = c.device_index(a), ib = c.device_index(b);
+      if (ia < 0 || ib < 0) throw ParseError("override: unknown device '" + (ia < 0 ? a : b) + "'");
+      if (ia == ib) throw ParseError("override: 'a' and 'b' must differ");
+      const double bw = positive(oj, "bandwidth_gbps", "override") * 1e9;
+      const double lat = nonneg(oj, "latency_us", "override") * 1e-6;
+      const std::pair<int, int> key = std::minmax(ia, ib);
+      auto it = ov.find(key);
+      if (it != ov.end() && (it->second.first != bw || it->second.second != lat))
+        throw ParseError("override: asymmetric bandwidth on pair '" + a + "'/'" + b + "'");
+      ov[key] = {bw, lat};
+    }
+  }
+  const size_t n = c.devices.size();
+  c.bandwidth.assign(n, std::vector<double>(n, 0.0));
+  c.latency.assign(n, std::vector<double>(n, 0.0));
+  for (size_t a = 0; a < n; ++a)
+    for (size_t b = a + 1; b < n; ++b) {
+      double bw = inter_bw, lat = inter_lat;
+      if (c.devices[a].machine == c.devices[b].machine) {
+        bw = machines[c.devices[a].machine].first;
+        lat = machines[c.devices[a].machine].second;
+      }
+      auto it = ov.find({int(a), int(b)});
+      if (it != ov.end()) {
+        bw = it->second.first;
+        lat = it->second.second;
+      }
+      c.bandwidth[a][b] = c.bandwidth[b][a] = bw;
+      c.latency[a][b] = c.latency[b][a] = lat;
+    }
   return c;
 }
 

@@ -37,6 +37,10 @@ struct Device {
 
 struct Cluster {
   std::vector<Device> devices;
+  // link matrices as json_io.cpp:149-171 expands them: same machine -> the
+  // machine's intra link, else the inter link, then per-pair overrides;
+  // bytes/s ("gbps" in the documents means GB/s, json_io.cpp:20) and seconds
+  std::vector<std::vector<double>> bandwidth, latency;
   int device_index(const std::string& id) const;
   double max_peak() const;
 };

@@ -40,6 +40,19 @@ class Plan:
     def world_size(self) -> int:
         return L.hexexec_plan_world_size(self._h)
 
+    def cost(self, state_multiplier: float = 1.0, extension: bool = False) -> dict:
+        """Reference cost model (cost_model.cpp:210-258) on this plan; with
+        extension=True uneven / mixed-speed TP stages are priced per rank."""
+        out = C.c_void_p()
+        err = L.errbuf()
+        L.check(L.hexexec_plan_cost(self._h, state_multiplier, 1 if extension else 0,
+                                    C.byref(out), err, len(err)), err)
+        return json.loads(L.take_string(out))
+
+    def mfu(self, seconds: float) -> float:
+        """Reference-convention MFU (cost_model.cpp:260-265) of a step time."""
+        return L.hexexec_plan_mfu(self._h, seconds)
+
     def close(self):
         if self._h:
             L.hexexec_plan_free(self._h)
