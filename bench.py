@@ -130,6 +130,16 @@ def gather_max(vals: list, rank: int, world: int, tag: str) -> list:
     return [max(v[i] for v in allv) for i in range(len(vals))]
 
 
+def gather_all(val, rank: int, world: int, tag: str) -> list:
+    """Every rank's JSON value, in rank order (TCPStore)."""
+    if world == 1:
+        return [val]
+    from paper_2409_01143_b200 import dist
+    st = dist.store(rank, world)
+    st.set(f"bench/{tag}/{rank}", json.dumps(val))
+    return [json.loads(st.get(f"bench/{tag}/{r}")) for r in range(world)]
+
+
 def gather_sum(vals: list, rank: int, world: int, tag: str) -> list:
     if world == 1:
         return vals
@@ -163,6 +173,11 @@ def run_plan(name: str, steps: int, warmup: int, rank: int, world: int, clocks: 
     ex.sync()
     st = ex.stats()
     ex.set_profile(False)
+    # closed-loop calibration input: this rank's effective layer speed
+    from paper_2409_01143_b200 import calibrate
+    speeds = gather_all([role["device"], calibrate.device_speed(st, role, json.loads(m), 2),
+                         st["sm_applied"] / max(st["sm_total"], 1)] if role["active"] else None,
+                        rank, world, f"cal-{name}")
     log(rank, f"{name}: warm-up {warmup}")
     for _ in range(warmup):      # first graph-mode step is captured into the CUDA graph
         ex.step_async()
@@ -204,7 +219,8 @@ def run_plan(name: str, steps: int, warmup: int, rank: int, world: int, clocks: 
     return dict(name=name, idx=idx, cluster=json.loads(c), model=json.loads(m),
                 plan=json.loads(p), dev_ms=dev_ms, e2e_ms=e2e_ms, loss=loss, clocks=clk,
                 stats=st, h2d=sums[0], d2h=sums[1], launches=sums[2], lin_flops=sums[3],
-                lin_ms=sums[4], lin_launches=sums[5], sm_share=sums[6])
+                lin_ms=sums[4], lin_launches=sums[5], sm_share=sums[6],
+                speeds=[x for x in speeds if x])
 
 
 def summarize(r: dict, steps: int, pk: dict) -> dict:
@@ -224,23 +240,38 @@ def summarize(r: dict, steps: int, pk: dict) -> dict:
             "aggregate_sm_share": r["sm_share"], "loss": r["loss"]}
 
 
-def reference_cost(name: str, seconds: float | None):
-    """Predicted step time / MFU of the plan by the compiled reference cost
-    model (oracle/_ref), when available; null for plans it cannot price."""
+def reference_cost(name: str, seconds: float | None, speeds=None):
+    """Predicted step time / MFU of the plan by the reference cost model
+    (cost_model.cpp:210-265, restated in the executor: Plan.cost, parity with
+    the compiled reference in tests/test_costmodel.py).  Mixed-speed TP plans,
+    which the reference formula refuses, are priced by the labelled per-rank
+    extension.  With `speeds` (closed-loop calibration) the
+    cluster's peak_tflops are replaced by the measured per-device speeds and
+    the calibrated prediction is compared with the measured step time."""
+    from paper_2409_01143_b200 import calibrate
+    from paper_2409_01143_b200.hexexec import HexexecError, Plan
+    c, m, p, _ = load(name)
+    out = {}
     try:
-        from oracle import refshim
-        if not refshim.available():
-            return None
-        c, m, p, _ = load(name)
-        res = refshim.check_plan(c, m, p)
-        if "cost" not in res:
-            return {"error": res.get("cost_error") or res.get("validate")}
-        out = {"predicted_s": res["cost"]["total"], "predicted_mfu": res["cost"]["mfu"]}
+        r = Plan(c, m, p).cost(1.0)
+        out = {"predicted_s": r["total"], "predicted_mfu": r["mfu"], "formula": "reference"}
+    except HexexecError as e:
+        r = Plan(c, m, p).cost(1.0, extension=True)
+        out = {"predicted_s": r["total"], "predicted_mfu": r["mfu"],
+               "formula": "extension (per-rank TP widths / speeds)", "reference_refuses": e.msg}
+    if seconds:
+        out["measured_s"] = seconds
+    if speeds:
+        cal = calibrate.calibrated_cluster(c, {d: v for d, v, _ in speeds},
+                                           {d: f for d, _, f in speeds})
+        rc = Plan(cal, m, p).cost(1.0, extension=True)
+        out["calibrated"] = {
+            "device_tflops": {d: round(v / 1e12, 1) for d, v, _ in speeds},
+            "predicted_s": rc["total"], "breakdown_s": {k: rc[k] for k in (
+                "compute", "tp_comm", "pp_comm", "dp_comm", "bubble")}}
         if seconds:
-            out["measured_s"] = seconds
-        return out
-    except Exception as e:  # noqa: BLE001
-        return {"error": str(e)}
+            out["calibrated"]["rel_error"] = (rc["total"] - seconds) / seconds
+    return out
 
 
 def cpu_reference(name: str, samples: int, warmup: int) -> dict:
@@ -382,7 +413,7 @@ def main():
         "sm_cap_rank0": {k: r["stats"].get(k) for k in ("sm_cap_mode", "sm_applied", "sm_total")},
         "clocks": r["clocks"],
         "cpu_baseline": cpu,
-        "reference_cost_model": reference_cost(asym, s["ms_per_step"] / 1e3),
+        "reference_cost_model": reference_cost(asym, s["ms_per_step"] / 1e3, r.get("speeds")),
         "loss": s["loss"],
     }
     print(json.dumps(line), flush=True)

@@ -4,16 +4,19 @@ Cluster and model documents follow the reference formats
 (/root/reference/proj/src/json_io.cpp:80-191) plus extension keys the
 reference parser ignores.  Planner plans (cfg3, cfg5, even-split baselines)
 are produced by the reference scheduler itself (oracle/_ref, built by
-oracle/Makefile) and committed, so nothing here runs on the GPU box.
+oracle/Makefile) and committed under configs/ as fixtures, so nothing here
+runs on the GPU box (test infrastructure: it is the only generator that
+links the compiled reference).
 
-    python configs/make_configs.py          # needs oracle/_ref/libhexplan_ref.so
+    python tests/golden/make_configs.py     # needs oracle/_ref/libhexplan_ref.so
 """
 import json
 import os
 import sys
 
-HERE = os.path.dirname(os.path.abspath(__file__))
-sys.path.insert(0, os.path.dirname(HERE))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+HERE = os.path.join(ROOT, "configs")
+sys.path.insert(0, ROOT)
 
 F, HALF, THIRD = 2250.0, 1125.0, 750.0
 
