@@ -614,22 +614,23 @@ struct BwdCfg {
   static constexpr uint32_t SMEM = 1024 + 6 * TILE + PDS + 2 * T * 4 + 256;
 };
 
-// P^T row kr of a query tile: pk (S^T in, P^T out, kept for the dS pass) and
-// the bf16 copy for the dV product; the causal mask only on the diagonal tile
+// P^T of key row kr over query columns [q0, q0 + 64): pk (S^T in, P^T out,
+// kept for the dS pass) and the bf16 copy for the dV product; the causal mask
+// only on the diagonal tile
 template <bool DIAG>
-HX_DEVICE void bwd_p_tile(float (&pk)[T], const float* sLse, float scale_log2, int kr,
+HX_DEVICE void bwd_p_cols(float (&pk)[T / 2], const float* sLse, float scale_log2, int kr, int q0,
                           uint8_t* sPD) {
 #pragma unroll
-  for (int q8 = 0; q8 < T / 8; ++q8) {
-    const float4 la = *reinterpret_cast<const float4*>(sLse + q8 * 8);
-    const float4 lb = *reinterpret_cast<const float4*>(sLse + q8 * 8 + 4);
+  for (int q8 = 0; q8 < T / 16; ++q8) {
+    const float4 la = *reinterpret_cast<const float4*>(sLse + q0 + q8 * 8);
+    const float4 lb = *reinterpret_cast<const float4*>(sLse + q0 + q8 * 8 + 4);
     const float ls[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
     float pr[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int qc = q8 * 8 + k;
       const float e = ex2(fmaf(pk[qc], scale_log2, -ls[k]));
-      pr[k] = (DIAG && kr > qc) ? 0.f : e;
+      pr[k] = (DIAG && kr > q0 + qc) ? 0.f : e;
       pk[qc] = pr[k];
     }
     uint4 w;
@@ -637,7 +638,7 @@ HX_DEVICE void bwd_p_tile(float (&pk)[T], const float* sLse, float scale_log2, i
     w.y = pack_bf16x2(pr[2], pr[3]);
     w.z = pack_bf16x2(pr[4], pr[5]);
     w.w = pack_bf16x2(pr[6], pr[7]);
-    *reinterpret_cast<uint4*>(sPD + kchunk(kr, q8)) = w;
+    *reinterpret_cast<uint4*>(sPD + kchunk(kr, q0 / 8 + q8)) = w;
   }
 }
 
@@ -647,8 +648,10 @@ HX_DEVICE uint64_t mnview(uint32_t base, int ks) {
   return umma_desc_sw128(base + ks * 2048, ATOM, 1024);
 }
 
+constexpr int kBwdThreads = 384;  // warps 0-3: TMA / MMA / TMEM alloc; 4-11: softmax
+
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                     const __grid_constant__ CUtensorMap tmDQ, const BwdParams p) {
@@ -704,13 +707,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(s_full, 1);
     mbar_init(dp_full, 1);
-    mbar_init(p_full, 4);
+    mbar_init(p_full, 8);
     mbar_init(pds_free, 1);
-    mbar_init(ds_full, 4);
+    mbar_init(ds_full, 8);
     mbar_init(dq_full, 1);
-    mbar_init(dq_empty, 4);
+    mbar_init(dq_empty, 8);
     mbar_init(dkv_full, 1);
-    mbar_init(s_read, 4);
+    mbar_init(s_read, 8);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(tslot);
@@ -798,13 +801,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_commit(dkv_full);
     }
   } else if (warp >= 4) {
-    const int ew = warp - 4;
-    const int tid = threadIdx.x - 128;          // 0..127
+    // eight softmax warps, two per SM sub-partition: warp (g, ew) owns TMEM
+    // lanes 32*ew.. (key rows) and query columns [64g, 64g+64) of P^T / dS^T,
+    // then dQ columns [g*D/2, (g+1)*D/2)
+    const int g = (warp - 4) / 4;
+    const int ew = (warp - 4) % 4;
+    const int tid = threadIdx.x - 128;          // 0..255
     const int kr = ew * 32 + lane;              // key row within the tile (TMEM lane)
     const uint32_t lane_off = uint32_t(ew * 32) << 16;
-    uint8_t* stage = sPD + ew * (32 * 64 * 4);  // dQ staging: [32 rows][64 fp32] per warp
+    const int q0 = g * (T / 2);                 // first query column of this warp
+    uint8_t* stage = sPD + (warp - 4) * 4096;   // dQ staging: [32 rows][32 fp32] per warp
     const long long z0 = ((long long)b * p.nh + h) * p.S + (long long)kt * T;
-    float nlse = p.lse[z0 + tid], ndel = p.delta[z0 + tid];  // prefetched statistics
+    const float* stat_src = tid < T ? p.lse : p.delta;
+    float* stat_dst = tid < T ? sLse : sDel;
+    const int si = tid % T;
+    float nstat = stat_src[z0 + si];            // prefetched statistic (lse or delta)
     for (int t = 0; t < ntiles; ++t) {
       const int i = kt + t;
       const bool diag = t == 0;
@@ -812,34 +823,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       // this warp's dQ reduce of tile t-1 must have read its staging area (the
       // staging areas overlap other warps' P rows) before anyone writes P_t
       if (lane == 0) bulk_wait_read<0>();
-      // per-query statistics of this tile, shared by the four warps
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      sLse[tid] = nlse;
-      sDel[tid] = ndel;
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (t + 1 < ntiles) {
-        nlse = p.lse[zq + T + tid];
-        ndel = p.delta[zq + T + tid];
-      }
-      // P^T, kept in registers for the dS pass
+      // per-query statistics of this tile, shared by the eight warps
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      stat_dst[si] = nstat;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (t + 1 < ntiles) nstat = stat_src[zq + T + si];
+      // P^T (64 query columns), kept in registers for the dS pass
       mbar_wait(s_full, t & 1);
       tc_fence_after();
-      uint32_t pu[T];
+      uint32_t pu[T / 2];
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        tmem_ld_32x32b_x32(tbase + lane_off + cS + uint32_t(c * 32),
+      for (int c = 0; c < 2; ++c)
+        tmem_ld_32x32b_x32(tbase + lane_off + cS + uint32_t(q0 + c * 32),
                            *reinterpret_cast<uint32_t(*)[32]>(pu + c * 32));
       tmem_ld_wait();
-      float pk[T];
+      float pk[T / 2];
 #pragma unroll
-      for (int k = 0; k < T; ++k) pk[k] = __uint_as_float(pu[k]);
+      for (int k = 0; k < T / 2; ++k) pk[k] = __uint_as_float(pu[k]);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(s_read);  // S region may take S_{t+1} now
       if (diag)
-        bwd_p_tile<true>(pk, sLse, p.scale_log2, kr, sPD);
+        bwd_p_cols<true>(pk, sLse, p.scale_log2, kr, q0, sPD);
       else
-        bwd_p_tile<false>(pk, sLse, p.scale_log2, kr, sPD);
+        bwd_p_cols<false>(pk, sLse, p.scale_log2, kr, q0, sPD);
       fence_async_shared();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
@@ -847,67 +854,67 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(dp_full, t & 1);
       mbar_wait(pds_free, t & 1);
       tc_fence_after();
+      uint32_t dv[T / 2];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t dv[32];
-        tmem_ld_32x32b_x32(tbase + lane_off + cP + uint32_t(c * 32), dv);
-        tmem_ld_wait();
+      for (int c = 0; c < 2; ++c)
+        tmem_ld_32x32b_x32(tbase + lane_off + cP + uint32_t(q0 + c * 32),
+                           *reinterpret_cast<uint32_t(*)[32]>(dv + c * 32));
+      tmem_ld_wait();
 #pragma unroll
-        for (int q8 = 0; q8 < 4; ++q8) {
-          float ds[8];
-          const float4 da = *reinterpret_cast<const float4*>(sDel + c * 32 + q8 * 8);
-          const float4 db = *reinterpret_cast<const float4*>(sDel + c * 32 + q8 * 8 + 4);
-          const float dl[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
+      for (int q8 = 0; q8 < T / 16; ++q8) {
+        float ds[8];
+        const float4 da = *reinterpret_cast<const float4*>(sDel + q0 + q8 * 8);
+        const float4 db = *reinterpret_cast<const float4*>(sDel + q0 + q8 * 8 + 4);
+        const float dl[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int qc = c * 32 + q8 * 8 + k;
-            ds[k] = pk[qc] * (__uint_as_float(dv[q8 * 8 + k]) - dl[k]) * p.scale;
-          }
-          uint4 w;
-          w.x = pack_bf16x2(ds[0], ds[1]);
-          w.y = pack_bf16x2(ds[2], ds[3]);
-          w.z = pack_bf16x2(ds[4], ds[5]);
-          w.w = pack_bf16x2(ds[6], ds[7]);
-          *reinterpret_cast<uint4*>(sPD + kchunk(kr, c * 4 + q8)) = w;
+        for (int k = 0; k < 8; ++k) {
+          const int qc = q8 * 8 + k;
+          ds[k] = pk[qc] * (__uint_as_float(dv[qc]) - dl[k]) * p.scale;
         }
+        uint4 w;
+        w.x = pack_bf16x2(ds[0], ds[1]);
+        w.y = pack_bf16x2(ds[2], ds[3]);
+        w.z = pack_bf16x2(ds[4], ds[5]);
+        w.w = pack_bf16x2(ds[6], ds[7]);
+        *reinterpret_cast<uint4*>(sPD + kchunk(kr, q0 / 8 + q8)) = w;
       }
       tc_fence_before();
       fence_async_shared();
       __syncwarp();
       if (lane == 0) mbar_arrive(ds_full);
-      // dQ_i partial (TMEM rows = queries) -> staged fp32 -> TMA reduce-add
+      // dQ_i partial (TMEM rows = queries) -> staged fp32 -> TMA reduce-add;
+      // this warp: D/2 columns in 32-column chunks through a 4 KB stage
       mbar_wait(dq_full, t & 1);
       tc_fence_after();
       const int qrow = i * T + ew * 32;  // first query row of this warp's slab
 #pragma unroll
-      for (int half = 0; half < D / 64; ++half) {
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(tbase + lane_off + cP + uint32_t(half * 64 + c * 32), v);
-          tmem_ld_wait();
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            *reinterpret_cast<float4*>(stage + c * 4096 + swz128(lane, q)) =
-                make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                            __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+      for (int c = 0; c < D / 64; ++c) {
+        const int col = g * (D / 2) + c * 32;
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tbase + lane_off + cP + uint32_t(col), v);
+        tmem_ld_wait();
+        if (c > 0) {
+          if (lane == 0) bulk_wait_read<0>();  // stage reused by the next chunk
+          __syncwarp();
         }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<float4*>(stage + swz128(lane, q)) =
+              make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                          __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
         fence_async_shared();
         __syncwarp();
         if (lane == 0) {
-          tma_reduce_add_4d(&tmDQ, stage, h * D + half * 64, b * p.S + qrow, 0, 0);
-          tma_reduce_add_4d(&tmDQ, stage + 4096, h * D + half * 64 + 32, b * p.S + qrow, 0, 0);
+          tma_reduce_add_4d(&tmDQ, stage, h * D + col, b * p.S + qrow, 0, 0);
           bulk_commit();
-          if (half + 1 < D / 64) bulk_wait_read<0>();  // staging reused by the next half
         }
-        __syncwarp();
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(dq_empty);
     }
     if (lane == 0) bulk_wait_all();
-    // dK, dV of this key tile -> bf16 into the dqkv buffer
+    // dK, dV of this key tile -> bf16 into the dqkv buffer (this warp: D/2 columns)
     mbar_wait(dkv_full, 0);
     tc_fence_after();
     const long long row = (long long)b * p.S + kt * T + kr;
@@ -916,14 +923,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int part = 0; part < 2; ++part) {
       const uint32_t col0 = part == 0 ? cK : cV;
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
+      for (int c = 0; c < D / 64; ++c) {
+        const int col = g * (D / 2) + c * 32;
         uint32_t v[32];
-        tmem_ld_32x32b_x32(tbase + lane_off + col0 + uint32_t(c * 32), v);
+        tmem_ld_32x32b_x32(tbase + lane_off + col0 + uint32_t(col), v);
         tmem_ld_wait();
         float f[32];
 #pragma unroll
         for (int k = 0; k < 32; ++k) f[k] = __uint_as_float(v[k]);
-        uint4* o = reinterpret_cast<uint4*>(dst + (part + 1) * D + c * 32);
+        uint4* o = reinterpret_cast<uint4*>(dst + (part + 1) * D + col);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           uint4 w;
@@ -1109,7 +1117,7 @@ cudaError_t launch_bwd(const AttnBwdDesc& a, cudaStream_t s) {
   p.scale = a.scale;
   p.scale_log2 = a.scale * 1.4426950408889634f;
   const int grid = (a.S / T) * a.nh * a.mb;
-  attn_bwd_kernel<D><<<grid, kThreads, C::SMEM, s>>>(q, k, v, dO, dq, p);
+  attn_bwd_kernel<D><<<grid, kBwdThreads, C::SMEM, s>>>(q, k, v, dO, dq, p);
   attn_dq_cast_kernel<D><<<ew_blocks(M * a.nh * (D / 8)), 256, 0, s>>>(a.dq_acc, a.dqkv, M, a.nh);
   return cudaGetLastError();
 }
