@@ -428,7 +428,7 @@ hexexec_status hexexec_k_ce(const float* logits, int Vr, int v0, const int32_t* 
   float* st2 = scratch + 2 * M;
   hexexec::k_ce_stats(logits, Vr, v0, tok, M, S, lmax, lsum, st2, s);
   hexexec::k_ce_finish(logits, Vr, v0, tok, M, S, lmax, st2, inv_count,
-                       static_cast<hexexec::bf16*>(dlogits), loss_acc, s);
+                       static_cast<hexexec::bf16*>(dlogits), loss_acc, scratch + 4 * M, s);
   return cuda_status(cudaGetLastError());
 }
 

@@ -75,6 +75,7 @@ ExecConfig parse_exec_config(const std::string& text) {
       else if (k == "dp_overlap") c.dp_overlap = v.get<bool>();
       else if (k == "gemm_split") c.gemm_split = v.get<bool>();
       else if (k == "recompute") c.recompute = v.get<bool>();
+      else if (k == "pp_protocol") c.pp_protocol = v.get<std::string>();
       else throw ParseError("exec config: unknown key '" + k + "'");
     } catch (const nlohmann::json::exception& e) {
       throw ParseError("exec config: bad value for '" + k + "'");
@@ -86,6 +87,8 @@ ExecConfig parse_exec_config(const std::string& text) {
     throw ParseError("exec config: attention must be fused|unfused");
   if (c.dp_comm_dtype != "bf16" && c.dp_comm_dtype != "fp32")
     throw ParseError("exec config: dp_comm_dtype must be bf16|fp32");
+  if (c.pp_protocol != "direct" && c.pp_protocol != "leader")
+    throw ParseError("exec config: pp_protocol must be direct|leader");
   return c;
 }
 
@@ -198,6 +201,7 @@ class Executor {
   float* gemm_ws_ = nullptr;  // zero between GEMMs (the kernel leaves it zero)
   int* gemm_cnt_ = nullptr;
   float* dg_part_ = nullptr;
+  uint32_t* embed_keys_ = nullptr;
   LayerActs rc_acts_{};  // recompute: the one shared activation set
   int32_t* tokens = nullptr;
   int32_t* tokens_pinned = nullptr;
@@ -288,6 +292,9 @@ class Executor {
       v0 = 64 * role.vocab_chunks.begin;
       mb = role.micro_batch;
       M = mb * S;
+      if (M > 16384)  // embedding-backward sort keys hold 16-bit positions
+        throw LimitExceeded("micro_batch * seq_len = " + std::to_string(M) +
+                            " tokens exceeds the 16384 per micro-batch limit");
       nl = role.layer_count;
       qkvw = 3 * d * nh;
       kr = d * nh;
@@ -454,11 +461,15 @@ class Executor {
     arena.reserve(M * H * 2);   // ypart
     arena.reserve(M * F * 2 + M * 2 * F * 2 + M * kr * 2 + M * qkvw * 2);
     arena.reserve(M * H * 4 * 2 + M * H * 2 + M * H * 2);  // dx ping-pong, dxb, dy16
-    if (role.last_stage) arena.reserve(M * Vr * 4 + 5 * M * 4);
+    if (role.last_stage) {
+      arena.reserve(M * Vr * 4);  // logits
+      arena.reserve(6 * M * 4);   // CE statistics + row losses
+    }
     arena.reserve(256);                                    // loss
     arena.reserve(kGemmWsBytes);                           // GEMM tail-split workspace
     arena.reserve(kGemmWsCounters * 4);
     arena.reserve(size_t(kRmsBwdCtas) * H * 4);             // rmsnorm bwd partial dg rows
+    arena.reserve(M * 4);                                  // embedding bwd sort keys
     arena.reserve(role.batch * (S + 1) * 4);               // tokens
     // memory tier: the device's memory_gib caps the rank (cost_model.cpp:130-153
     // applies the same per-device budget to its layer-memory estimate)
@@ -510,6 +521,7 @@ class Executor {
     gemm_ws_ = arena.take<float>(kGemmWsBytes / 4);
     gemm_cnt_ = arena.take<int>(kGemmWsCounters);
     dg_part_ = arena.take<float>(size_t(kRmsBwdCtas) * H);
+    embed_keys_ = arena.take<uint32_t>(M);
     ypart = arena.take<bf16>(M * H);
     da = arena.take<bf16>(M * F);
     dgu = arena.take<bf16>(M * 2 * F);
@@ -521,7 +533,7 @@ class Executor {
     dy16 = arena.take<bf16>(M * H);
     if (role.last_stage) {
       logits = arena.take<float>(M * Vr);
-      ce_scr = arena.take<float>(5 * M);
+      ce_scr = arena.take<float>(6 * M);
     }
     loss_acc = arena.take<float>(32);
     sp_ = reinterpret_cast<StepParams*>(loss_acc + 16);
@@ -844,7 +856,7 @@ class Executor {
     }
     const float inv_count = 1.f / float(role.batch * S);
     k_ce_finish(logits, int(Vr), int(v0), tk, int(M), int(S), gmax, st2, inv_count, sl.dlogits,
-                loss_acc, stream);
+                loss_acc, ce_scr + 5 * M, stream);
     kcheck("ce_finish");
   }
 
@@ -1012,7 +1024,7 @@ class Executor {
       group_ready(int(role.layer_start + l));
     }
     if (role.first_stage) {
-      k_embed_bwd(tok_of(mbi), cur, embed.g32, int(M), int(S), int(H), stream);
+      k_embed_bwd(tok_of(mbi), cur, embed.g32, int(M), int(S), int(H), embed_keys_, stream);
       kcheck("embed_bwd");
       group_ready(kGroupEmbed);
     }
@@ -1020,30 +1032,33 @@ class Executor {
   }
 
   // ------------------------------------------------------------ PP comm
-  void send_fwd(Slot& sl) {
-    for (int peer : role.fwd_send_to) {
-      HX_NCCL(ncclSend(sl.x[size_t(nl)], size_t(M * H), ncclFloat32, peer, world_comm, stream));
+  // leader protocol: only tp_index 0 talks to the neighbouring stage (whose
+  // first device is the first entry of the send lists), then broadcasts
+  bool pp_leader() const { return cfg.pp_protocol == "leader"; }
+  void send_to(const std::vector<int>& peers, const float* buf) {
+    for (size_t k = 0; k < peers.size(); ++k) {
+      if (pp_leader() && (role.tp_index != 0 || k > 0)) break;
+      HX_NCCL(ncclSend(buf, size_t(M * H), ncclFloat32, peers[k], world_comm, stream));
       ++nccl_calls_step;
     }
   }
-  void recv_fwd(Slot& sl) {
-    if (role.fwd_recv_from >= 0) {
-      HX_NCCL(ncclRecv(sl.x[0], size_t(M * H), ncclFloat32, role.fwd_recv_from, world_comm, stream));
-      ++nccl_calls_step;
-    }
+  void recv_from(int peer, float* buf) {
+    if (peer < 0 || (pp_leader() && role.tp_index != 0)) return;
+    HX_NCCL(ncclRecv(buf, size_t(M * H), ncclFloat32, peer, world_comm, stream));
+    ++nccl_calls_step;
   }
-  void send_bwd(const float* g) {
-    for (int peer : role.bwd_send_to) {
-      HX_NCCL(ncclSend(g, size_t(M * H), ncclFloat32, peer, world_comm, stream));
-      ++nccl_calls_step;
-    }
+  // leader protocol, after the receive has completed (outside the P2P group)
+  void bcast_in_stage(int peer, float* buf) {
+    if (peer < 0 || !pp_leader() || role.tp <= 1) return;
+    HX_NCCL(ncclBroadcast(buf, buf, size_t(M * H), ncclFloat32, 0, tp_comm(), stream));
+    ++nccl_calls_step;
   }
-  void recv_bwd(float* g) {
-    if (role.bwd_recv_from >= 0) {
-      HX_NCCL(ncclRecv(g, size_t(M * H), ncclFloat32, role.bwd_recv_from, world_comm, stream));
-      ++nccl_calls_step;
-    }
-  }
+  void send_fwd(Slot& sl) { send_to(role.fwd_send_to, sl.x[size_t(nl)]); }
+  void recv_fwd(Slot& sl) { recv_from(role.fwd_recv_from, sl.x[0]); }
+  void bcast_fwd(Slot& sl) { bcast_in_stage(role.fwd_recv_from, sl.x[0]); }
+  void send_bwd(const float* g) { send_to(role.bwd_send_to, g); }
+  void recv_bwd(float* g) { recv_from(role.bwd_recv_from, g); }
+  void bcast_bwd(float* g) { bcast_in_stage(role.bwd_recv_from, g); }
 
   // ------------------------------------------------------------ step
   bool accum_first_ = true;
@@ -1072,12 +1087,16 @@ class Executor {
     for (int64_t i = 0; i < warm; ++i) {
       Slot& sl = slot_of(i);
       recv_fwd(sl);
+      bcast_fwd(sl);
       if (pp) mark("nccl_pp");
       forward(i, sl);
       send_fwd(sl);
       if (pp) mark("nccl_pp");
     }
-    if (rem > 0) recv_fwd(slot_of(warm));
+    if (rem > 0) {
+      recv_fwd(slot_of(warm));
+      bcast_fwd(slot_of(warm));
+    }
     if (pp) mark("nccl_pp");
     for (int64_t i = 0; i < rem; ++i) {
       const int64_t f = warm + i;
@@ -1088,16 +1107,19 @@ class Executor {
       send_fwd(sl);
       recv_bwd(grecv);
       HX_NCCL(ncclGroupEnd());
+      bcast_bwd(grecv);
       if (pp) mark("nccl_pp");
       do_bwd(i);
       HX_NCCL(ncclGroupStart());
       send_bwd(bwd_out_);
       if (i + 1 < rem) recv_fwd(slot_of(f + 1));
       HX_NCCL(ncclGroupEnd());
+      if (i + 1 < rem) bcast_fwd(slot_of(f + 1));
       if (pp) mark("nccl_pp");
     }
     for (int64_t i = rem; i < n; ++i) {
       recv_bwd(grecv);
+      bcast_bwd(grecv);
       if (pp) mark("nccl_pp");
       do_bwd(i);
       send_bwd(bwd_out_);

@@ -29,6 +29,11 @@ struct ExecConfig {
   // micro-batch slot and re-run the layer forward (minus its output GEMM)
   // before the layer backward, into one shared activation set
   bool recompute = false;
+  // PP hand-off (cost_model.cpp:59-76): "direct" = every rank of
+  // the receiving stage gets its copy from a sender rank; "leader" = the
+  // stages' first devices exchange it and the receiving leader broadcasts it
+  // over its TP communicator (for links where only leaders are well connected)
+  std::string pp_protocol = "direct";
 };
 
 ExecConfig parse_exec_config(const std::string& text);

@@ -74,14 +74,57 @@ __global__ void embed_fwd_kernel(const int32_t* tok, const float* E, float* x, i
   for (int i = threadIdx.x; i < H / 4; i += blockDim.x) dst[i] = src[i];
 }
 
-__global__ void embed_bwd_kernel(const int32_t* tok, const float* dx, float* dE, int M, int S,
-                                 int H) {
-  int row = blockIdx.x;
-  if (row >= M) return;
-  int t = tok[(row / S) * (S + 1) + row % S];
-  float* dst = dE + (long long)t * H;
-  const float* src = dx + (long long)row * H;
-  for (int i = threadIdx.x; i < H; i += blockDim.x) atomicAdd(dst + i, src[i]);
+// Embedding backward, deterministic: (1) one CTA sorts the micro-batch's
+// (token, position) keys in shared memory (bitonic, M <= kEmbedSortMax);
+// (2) the CTA at the start of each run of equal tokens sums those rows in
+// position order and adds the sum to the token's dE row -- no atomics, so the
+// gradient is bitwise reproducible (repeated tokens are common).
+constexpr int kEmbedSortMax = 16384;
+
+__global__ void __launch_bounds__(1024) embed_sort_kernel(const int32_t* tok, int M, int S,
+                                                          uint32_t* keys) {
+  extern __shared__ uint32_t sk[];
+  int n = 1;
+  while (n < M) n <<= 1;
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    sk[i] = i < M ? (uint32_t(tok[(i / S) * (S + 1) + i % S]) << 16) | uint32_t(i) : 0xffffffffu;
+  __syncthreads();
+  for (int k = 2; k <= n; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const uint32_t a = sk[i], b = sk[l];
+          const bool up = (i & k) == 0;
+          if ((a > b) == up) {
+            sk[i] = b;
+            sk[l] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < M; i += blockDim.x) keys[i] = sk[i];
+}
+
+__global__ void embed_segsum_kernel(const uint32_t* __restrict__ keys, const float* __restrict__ dx,
+                                    float* __restrict__ dE, int M, int H) {
+  const int i = blockIdx.x;
+  const uint32_t tk = keys[i] >> 16;
+  if (i > 0 && (keys[i - 1] >> 16) == tk) return;  // not the start of a run
+  int end = i + 1;
+  while (end < M && (keys[end] >> 16) == tk) ++end;
+  float* dst = dE + (long long)tk * H;
+  for (int c = threadIdx.x * 4; c < H; c += blockDim.x * 4) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int r = i; r < end; ++r) {
+      const float4 v = *reinterpret_cast<const float4*>(dx + (long long)(keys[r] & 0xffffu) * H + c);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    float4 d = *reinterpret_cast<float4*>(dst + c);
+    d.x += acc.x; d.y += acc.y; d.z += acc.z; d.w += acc.w;
+    *reinterpret_cast<float4*>(dst + c) = d;
+  }
 }
 
 // ------------------------------------------------------------------ rmsnorm
@@ -552,7 +595,7 @@ __global__ void ce_rescale_kernel(const float* lmax, const float* lsum, const fl
 __global__ void ce_finish_kernel(const float* __restrict__ logits, int Vr, int v0,
                                  const int32_t* __restrict__ tok, int M, int S,
                                  const float* __restrict__ gmax, const float* __restrict__ st2,
-                                 float inv_count, bf16* __restrict__ dl, float* loss_acc) {
+                                 float inv_count, bf16* __restrict__ dl, float* row_loss) {
   int row = blockIdx.x;
   const float* l = logits + (long long)row * Vr;
   bf16* d = dl + (long long)row * Vr;
@@ -572,8 +615,23 @@ __global__ void ce_finish_kernel(const float* __restrict__ logits, int Vr, int v
   }
   if (threadIdx.x == 0 && v0 == 0) {
     // loss counted once per row, on the rank owning vocab offset 0
-    float loss = logf(st2[2 * row]) + m - st2[2 * row + 1];
-    atomicAdd(loss_acc, loss);
+    row_loss[row] = logf(st2[2 * row]) + m - st2[2 * row + 1];
+  }
+}
+
+// loss_acc += sum of the row losses in a fixed order (one CTA; deterministic)
+__global__ void __launch_bounds__(1024) loss_sum_kernel(const float* __restrict__ row_loss, int M,
+                                                        float* loss_acc) {
+  __shared__ float red[32];
+  float acc = 0.f;
+  for (int i = threadIdx.x; i < M; i += blockDim.x) acc += row_loss[i];
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = red[threadIdx.x];
+    v = warp_sum(v);
+    if (threadIdx.x == 0) *loss_acc += v;
   }
 }
 
@@ -689,8 +747,18 @@ void k_embed_fwd(const int32_t* tok, const float* E, float* x, int M, int S, int
   if (M > 0) embed_fwd_kernel<<<M, 256, 0, s>>>(tok, E, x, M, S, H);
 }
 void k_embed_bwd(const int32_t* tok, const float* dx, float* dE, int M, int S, int H,
-                 cudaStream_t s) {
-  if (M > 0) embed_bwd_kernel<<<M, 256, 0, s>>>(tok, dx, dE, M, S, H);
+                 uint32_t* keys, cudaStream_t s) {
+  if (M <= 0) return;
+  int n = 1;
+  while (n < M) n <<= 1;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(embed_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kEmbedSortMax * 4);
+    attr = true;
+  }
+  embed_sort_kernel<<<1, 1024, size_t(n) * 4, s>>>(tok, M, S, keys);
+  embed_segsum_kernel<<<M, 256, 0, s>>>(keys, dx, dE, M, H);
 }
 // H <= 4 * 2048 (checked by the executor's model validation)
 void k_rmsnorm_fwd(const float* x, const bf16* y, float* xo, const float* g, bf16* out,
@@ -776,9 +844,10 @@ void k_ce_rescale(const float* lmax, const float* lsum, const float* gmax, float
 }
 void k_ce_finish(const float* logits, int Vr, int v0, const int32_t* tok, int M, int S,
                  const float* gmax, const float* st2, float inv_count, bf16* dl,
-                 float* loss_acc, cudaStream_t s) {
-  if (M > 0)
-    ce_finish_kernel<<<M, 256, 0, s>>>(logits, Vr, v0, tok, M, S, gmax, st2, inv_count, dl, loss_acc);
+                 float* loss_acc, float* row_loss, cudaStream_t s) {
+  if (M <= 0) return;
+  ce_finish_kernel<<<M, 256, 0, s>>>(logits, Vr, v0, tok, M, S, gmax, st2, inv_count, dl, row_loss);
+  if (v0 == 0) loss_sum_kernel<<<1, 1024, 0, s>>>(row_loss, M, loss_acc);
 }
 void k_scale_cast(const float* g, bf16* out, long long n, float scale, cudaStream_t s) {
   if (n > 0) scale_cast_kernel<<<ew_grid(n, 4), 256, 0, s>>>(g, out, n, scale);

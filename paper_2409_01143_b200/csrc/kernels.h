@@ -63,8 +63,10 @@ void k_gen_tokens(int32_t* tok, long long n_samples, int S, long long sample0, u
 // x[m, :] = E[tok(m), :]  (tok row stride S+1)
 void k_embed_fwd(const int32_t* tok, const float* E, float* x, int M, int S, int H,
                  cudaStream_t s);
+// dE[tok(m), :] += dx[m, :], deterministic (sorted runs, no atomics); keys:
+// M uint32 scratch; M <= 16384 and position < 65536, token < 65536
 void k_embed_bwd(const int32_t* tok, const float* dx, float* dE, int M, int S, int H,
-                 cudaStream_t s);
+                 uint32_t* keys, cudaStream_t s);
 
 // xo = x (+ y);  out = bf16(xo * rstd * g);  rstd[m] saved.  xo may alias x only if y==null.
 void k_rmsnorm_fwd(const float* x, const bf16* y, float* xo, const float* g, bf16* out,
@@ -104,9 +106,10 @@ void k_ce_stats(const float* logits, int Vr, int v0, const int32_t* tok, int M, 
 void k_ce_rescale(const float* lmax, const float* lsum, const float* gmax, float* st2, int M,
                   cudaStream_t s);
 // dlogits = (softmax - onehot) * inv_count (bf16); loss_acc += sum_m (log(sum)+gmax - tlogit)
+// (row losses in row_loss[M], summed in a fixed order: reproducible)
 void k_ce_finish(const float* logits, int Vr, int v0, const int32_t* tok, int M, int S,
                  const float* gmax, const float* st2, float inv_count, bf16* dlogits,
-                 float* loss_acc, cudaStream_t s);
+                 float* loss_acc, float* row_loss, cudaStream_t s);
 
 // DP gradient prep: out = bf16(scale * g)
 void k_scale_cast(const float* g, bf16* out, long long n, float scale, cudaStream_t s);

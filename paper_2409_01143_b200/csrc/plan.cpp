@@ -198,6 +198,7 @@ Model parse_model_doc(const std::string& text) {
   if (m.hidden_dim > 8192) throw InvalidArgument("model: hidden_dim must be <= 8192");
   if (m.ffn_dim % 64 != 0) throw InvalidArgument("model: ffn_dim must be a multiple of 64");
   if (m.vocab_size % 64 != 0) throw InvalidArgument("model: vocab_size must be a multiple of 64");
+  if (m.vocab_size > 65536) throw InvalidArgument("model: vocab_size must be <= 65536");
   if (m.seq_len % 128 != 0) throw InvalidArgument("model: seq_len must be a multiple of 128");
   return m;
 }

@@ -138,3 +138,14 @@ def test_recompute_matches_stored_activations(tmp_path, name):
         for key in a:
             if key.endswith("|w"):
                 assert np.allclose(a[key], b[key], rtol=1e-6, atol=1e-7), key
+
+
+@pytest.mark.parametrize("name", ["tiny_pp3_4", "tiny_mixed4"])
+def test_leader_pp_protocol(tmp_path, name):
+    """Leader-GPU send -> in-stage broadcast PP hand-off: same
+    step as the direct per-rank hand-off, and parity with the oracle."""
+    direct = run_plan(name, tmp_path / "direct", steps=2)
+    leader = run_plan(name, tmp_path / "leader", steps=2, xcfg={"pp_protocol": "leader"})
+    check_against_oracle(name, leader)
+    for a, b in zip(direct, leader):
+        assert np.allclose(a["losses"], b["losses"], rtol=1e-6, atol=0)
