@@ -404,7 +404,8 @@ def main():
                      "achieved": achieved, "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
                      "frac": achieved / pk["bf16_tflops_sustained"] if achieved else None,
                      "peak_kind": "sustained (kernel timed inside a long step)",
-                     "launches_per_step": r["lin_launches"],
+                     "launches_per_step": r["lin_launches"] / max(
+                         r["stats"].get("gemm_profile", {}).get("steps", 1), 1),
                      "algorithmic_flops_per_launch": lin_flops_launch,
                      "avg_launch_ms": lin_ms_launch, "traffic": traffic},
         "gemm_profile_rank0": r["stats"].get("gemm_profile"),

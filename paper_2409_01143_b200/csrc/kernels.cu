@@ -375,24 +375,24 @@ __global__ void __launch_bounds__(kNormThreads, NC <= 2 ? 2 : 1)
 }
 
 // dg[j] += sum of the CTA partial rows, in a fixed order (deterministic):
-// block = 32 columns x 8 row groups; group g sums rows g, g+8, ... then the
-// 8 group sums are added in group order
-__global__ void colsum_add_kernel(const float* __restrict__ part, int rows, int H,
-                                  float* __restrict__ dg) {
-  __shared__ float red[8][33];
+// block = 32 columns x 32 row groups; group g sums rows g, g+32, ... then the
+// 32 group sums are added in group order
+__global__ void __launch_bounds__(1024) colsum_add_kernel(const float* __restrict__ part, int rows,
+                                                          int H, float* __restrict__ dg) {
+  __shared__ float red[32][33];
   const int j = blockIdx.x * 32 + (threadIdx.x & 31);
   const int grp = threadIdx.x >> 5;
   float s = 0.f;
   if (j < H) {
 #pragma unroll 4
-    for (int r = grp; r < rows; r += 8) s += part[(long long)r * H + j];
+    for (int r = grp; r < rows; r += 32) s += part[(long long)r * H + j];
   }
   red[grp][threadIdx.x & 31] = s;
   __syncthreads();
   if (grp == 0 && j < H) {
     float t = red[0][threadIdx.x];
 #pragma unroll
-    for (int g = 1; g < 8; ++g) t += red[g][threadIdx.x];
+    for (int g = 1; g < 32; ++g) t += red[g][threadIdx.x];
     dg[j] += t;
   }
 }
@@ -811,7 +811,7 @@ void k_rmsnorm_bwd(const bf16* dyb, const float* dyf, const float* x, const floa
   }
 #undef HX_NORM_BWD_NC
 #undef HX_NORM_BWD
-  colsum_add_kernel<<<(H + 31) / 32, 256, 0, s>>>(dg_part, grid, H, dg);
+  colsum_add_kernel<<<(H + 31) / 32, 1024, 0, s>>>(dg_part, grid, H, dg);
 }
 void k_rope(bf16* qkv, int M, int S, int nh, int d, float theta, int inverse, cudaStream_t s) {
   long long n = (long long)M * ((nh + kRopeHeads - 1) / kRopeHeads) * (d / 16);
