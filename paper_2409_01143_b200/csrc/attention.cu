@@ -679,7 +679,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* dq_empty = bar + 11;
   uint64_t* dkv_full = bar + 12;
   uint64_t* s_read = bar + 13;     // softmax warps hold S_t in registers
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 14);
+  uint64_t* dq_issued = bar + 14;  // [2] softmax warps have issued their dQ_t reduce-adds
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 16);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -714,6 +715,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(dq_empty, 8);
     mbar_init(dkv_full, 1);
     mbar_init(s_read, 8);
+    mbar_init(&dq_issued[0], 8);
+    mbar_init(&dq_issued[1], 8);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(tslot);
@@ -733,6 +736,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int i = kt + t;
         const int slot = t & 1;
         mbar_wait(&qdo_empty[slot], ((t >> 1) & 1) ^ 1);
+        // let the dQ reduce-adds of tile t-2 enter the TMA queue ahead of this
+        // tile's 2 x TILE loads (they are on the softmax warps' critical path)
+        // (one barrier per slot parity: tile t cannot complete before this load,
+        // so a barrier is never two phases ahead of its waiter)
+        if (t >= 2) mbar_wait(&dq_issued[slot], ((t - 2) >> 1) & 1);
         mbar_arrive_expect_tx(&qdo_full[slot], 2 * C::TILE);
         for (int a = 0; a < DA; ++a) {
           tma_load_4d(sQ + slot * C::TILE + a * ATOM, &tmQ, &qdo_full[slot], a * 64, i * T, h, b);
@@ -854,29 +862,27 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_wait(dp_full, t & 1);
       mbar_wait(pds_free, t & 1);
       tc_fence_after();
-      uint32_t dv[T / 2];
 #pragma unroll
-      for (int c = 0; c < 2; ++c)
-        tmem_ld_32x32b_x32(tbase + lane_off + cP + uint32_t(q0 + c * 32),
-                           *reinterpret_cast<uint32_t(*)[32]>(dv + c * 32));
-      tmem_ld_wait();
+      for (int c = 0; c < 2; ++c) {
+        uint32_t dv[32];
+        tmem_ld_32x32b_x32(tbase + lane_off + cP + uint32_t(q0 + c * 32), dv);
+        tmem_ld_wait();
 #pragma unroll
-      for (int q8 = 0; q8 < T / 16; ++q8) {
-        float ds[8];
-        const float4 da = *reinterpret_cast<const float4*>(sDel + q0 + q8 * 8);
-        const float4 db = *reinterpret_cast<const float4*>(sDel + q0 + q8 * 8 + 4);
-        const float dl[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
+        for (int q8 = 0; q8 < 4; ++q8) {
+          float ds[8];
+          const float4 da = *reinterpret_cast<const float4*>(sDel + q0 + c * 32 + q8 * 8);
+          const float4 db = *reinterpret_cast<const float4*>(sDel + q0 + c * 32 + q8 * 8 + 4);
+          const float dl[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int qc = q8 * 8 + k;
-          ds[k] = pk[qc] * (__uint_as_float(dv[qc]) - dl[k]) * p.scale;
+          for (int k = 0; k < 8; ++k)
+            ds[k] = pk[c * 32 + q8 * 8 + k] * (__uint_as_float(dv[q8 * 8 + k]) - dl[k]) * p.scale;
+          uint4 w;
+          w.x = pack_bf16x2(ds[0], ds[1]);
+          w.y = pack_bf16x2(ds[2], ds[3]);
+          w.z = pack_bf16x2(ds[4], ds[5]);
+          w.w = pack_bf16x2(ds[6], ds[7]);
+          *reinterpret_cast<uint4*>(sPD + kchunk(kr, q0 / 8 + c * 4 + q8)) = w;
         }
-        uint4 w;
-        w.x = pack_bf16x2(ds[0], ds[1]);
-        w.y = pack_bf16x2(ds[2], ds[3]);
-        w.z = pack_bf16x2(ds[4], ds[5]);
-        w.w = pack_bf16x2(ds[6], ds[7]);
-        *reinterpret_cast<uint4*>(sPD + kchunk(kr, q0 / 8 + q8)) = w;
       }
       tc_fence_before();
       fence_async_shared();
@@ -911,7 +917,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(dq_empty);
+      if (lane == 0) {
+        mbar_arrive(dq_empty);
+        mbar_arrive(&dq_issued[t & 1]);
+      }
     }
     if (lane == 0) bulk_wait_all();
     // dK, dV of this key tile -> bf16 into the dqkv buffer (this warp: D/2 columns)
