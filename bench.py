@@ -19,6 +19,7 @@ inside the timed region (host wall clock, max over ranks).
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import statistics
@@ -33,10 +34,12 @@ sys.path.insert(0, ROOT)
 CFG = os.path.join(ROOT, "configs")
 
 METRIC = "tokens/s & MFU per asym plan at 1/2/4/8 B200 vs even split + CPU ref"
-# N -> (asymmetric plan, even-split plan at equal aggregate compute)
+# N -> (asymmetric plan, even-split plans at equal aggregate compute: the first
+# keeps the asymmetric plan's parallel structure with even shares on a
+# homogeneous cluster; the next is the reference's symmetric_baseline shape)
 PLANS = {
     1: ("llama7b_4l_1gpu", None),
-    2: ("llama7b_4l_tp31", "llama7b_4l_2_even"),
+    2: ("llama7b_4l_tp31", "llama7b_4l_tp11_eq,llama7b_4l_2_even"),
     4: ("llama7b_4l_4_asym", "llama7b_4l_4_even"),
     8: ("llama7b_8_asym", "llama7b_8_eq_even"),
 }
@@ -78,21 +81,34 @@ def model_flops(m: dict, tokens: int) -> tuple[float, float]:
 class Clocks:
     """nvidia-smi sampler for the timed region (rank 0)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self):
+    def __init__(self, n_gpus: int = 1):
+        # the job's GPUs only (an idle GPU of the box would drag the median down)
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        ids = [x.strip() for x in vis.split(",")] if vis else [str(i) for i in range(n_gpus)]
+        self.ids = ",".join(ids[:n_gpus])
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         self.p = None
+        self.t0 = self.t1 = None
 
     def start(self):
+        """Start sampling (before the warm-up: nvidia-smi takes ~1 s to come up);
+        only rows stamped inside [mark_begin, mark_end] are kept."""
         try:
-            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+            self.p = subprocess.Popen(["nvidia-smi", "-i", self.ids, f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
+
+    def mark_begin(self):
+        self.t0 = datetime.datetime.now()
+
+    def mark_end(self):
+        self.t1 = datetime.datetime.now()
 
     def stop(self) -> dict:
         if self.p is None:
@@ -106,12 +122,15 @@ class Clocks:
         for r in rows:
             r = [x.strip() for x in r]
             try:
-                sm.append(float(r[1]))
-                mx.append(float(r[2]))
+                ts = datetime.datetime.strptime(r[0], "%Y/%m/%d %H:%M:%S.%f")
+                if self.t0 and self.t1 and not (self.t0 <= ts <= self.t1):
+                    continue
+                sm.append(float(r[2]))
+                mx.append(float(r[3]))
             except (ValueError, IndexError):
                 continue
             for i, n in enumerate(names):
-                if len(r) > 5 + i and r[5 + i].lower() == "active":
+                if len(r) > 6 + i and r[6 + i].lower() == "active":
                     reasons.add(n)
         os.unlink(self.f.name)
         return {"sm_mhz": statistics.median(sm) if sm else None,
@@ -161,7 +180,11 @@ def run_plan(name: str, steps: int, warmup: int, rank: int, world: int, clocks: 
     from paper_2409_01143_b200 import dist
     c, m, p, idx = load(name)
     log(rank, f"{name}: creating executor")
-    ex = dist.make_executor(c, m, p, dict(EXEC_CFG), tag=f"uid-{name}")
+    # per-GEMM CUDA events inside the step graph (one micro-batch per step):
+    # the roofline is read from the timed replays themselves
+    xc = {"graph_gemm_events": True}
+    xc.update(EXEC_CFG)
+    ex = dist.make_executor(c, m, p, xc, tag=f"uid-{name}")
     role = ex.role
     # ---- profiled pass first (eager, CUDA events around every GEMM and after every
     # op): roofline evidence for the TP GEMMs + per-kernel-class step timeline.
@@ -178,6 +201,9 @@ def run_plan(name: str, steps: int, warmup: int, rank: int, world: int, clocks: 
     speeds = gather_all([role["device"], calibrate.device_speed(st, role, json.loads(m), 2),
                          st["sm_applied"] / max(st["sm_total"], 1)] if role["active"] else None,
                         rank, world, f"cal-{name}")
+    ck = Clocks(world) if clocks else None
+    if ck:
+        ck.start()
     log(rank, f"{name}: warm-up {warmup}")
     for _ in range(warmup):      # first graph-mode step is captured into the CUDA graph
         ex.step_async()
@@ -185,15 +211,18 @@ def run_plan(name: str, steps: int, warmup: int, rank: int, world: int, clocks: 
     log(rank, f"{name}: timed {steps}")
     # ---- device-timed region (tokens resident in HBM)
     dist.barrier(rank, world, f"t0-{name}")
-    ck = Clocks() if clocks else None
     if ck:
-        ck.start()
+        ck.mark_begin()
     ex.timer_start()
     for _ in range(steps):
         ex.step_async()
     dev_ms = ex.timer_stop()
+    if ck:
+        ck.mark_end()
     clk = ck.stop() if ck else None
-    launches_step = ex.stats().get("launches_last_step", 0)
+    ex.sync()  # reads the per-GEMM events of the last timed replay
+    st_timed = ex.stats()
+    launches_step = st_timed.get("launches_last_step", 0)
     dev_ms = gather_max([dev_ms], rank, world, f"dev-{name}")[0]
     # ---- e2e region: public API with host token buffers (H2D) + loss (D2H)
     log(rank, f"{name}: e2e {steps}")
@@ -214,12 +243,20 @@ def run_plan(name: str, steps: int, warmup: int, rank: int, world: int, clocks: 
                        float(st["sm_applied"]) / max(float(st["sm_total"]), 1.0)
                        if role["active"] else 0.0],
                       rank, world, f"sum-{name}")
+    gg = st_timed.get("gemm_profile_graph")
+    if gg:  # roofline from inside the timed region (events captured in the graph)
+        lin = gg.get("tp_linear", {})
+    share = float(st["sm_applied"]) / max(float(st["sm_total"]), 1.0) if role["active"] else 0.0
+    tl_all = gather_all({k: round(v["ms"] / 2, 3) for k, v in st.get("timeline_ms", {}).items()},
+                        rank, world, f"tl-{name}")
+    per_rank = gather_all([float(lin.get("flops", 0.0)), float(lin.get("ms", 0.0)),
+                           float(lin.get("launches", 0)), share], rank, world, f"lin-{name}")
     ex.close()
     log(rank, f"{name}: done")
     return dict(name=name, idx=idx, cluster=json.loads(c), model=json.loads(m),
                 plan=json.loads(p), dev_ms=dev_ms, e2e_ms=e2e_ms, loss=loss, clocks=clk,
-                stats=st, h2d=sums[0], d2h=sums[1], launches=sums[2], lin_flops=sums[3],
-                lin_ms=sums[4], lin_launches=sums[5], sm_share=sums[6],
+                stats=st, gemm_graph=gg, h2d=sums[0], d2h=sums[1], launches=sums[2], lin_flops=sums[3],
+                lin_ms=sums[4], lin_launches=sums[5], sm_share=sums[6], lin_per_rank=per_rank, tl_all=tl_all,
                 speeds=[x for x in speeds if x])
 
 
@@ -318,10 +355,11 @@ def cpu_reference(name: str, samples: int, warmup: int) -> dict:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--plan", default=None, help="configs/plans/<name>.json (asymmetric arm)")
-    ap.add_argument("--even", default=None, help="even-split comparison plan ('none' to skip)")
+    ap.add_argument("--even-plans", default=None,
+                    help="comma-separated even-split comparison plans ('none' to skip)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--exec-config", default="{}", help="JSON executor config overrides")
@@ -335,8 +373,8 @@ def main():
     if a.plan:
         asym = a.plan
         even = None
-    if a.even:
-        even = None if a.even == "none" else a.even
+    if a.even_plans:
+        even = None if a.even_plans == "none" else a.even_plans
     if asym is None:
         raise SystemExit(f"no default plan for {a.gpus} GPUs; pass --plan")
     _, m_doc, _, _ = load(asym)
@@ -370,14 +408,25 @@ def main():
     r = run_plan(asym, a.steps, a.warmup, rank, world, clocks=(rank == 0))
     s = summarize(r, a.steps, pk)
     ev = None
-    if even:
-        re_ = run_plan(even, a.steps, a.warmup, rank, world, clocks=False)
-        ev = summarize(re_, a.steps, pk)
+    evs = []
+    for e_name in (even.split(",") if even else []):
+        re_ = run_plan(e_name, a.steps, a.warmup, rank, world, clocks=False)
+        evs.append(summarize(re_, a.steps, pk))
+    ev = evs[0] if evs else None
     if rank != 0:
         return
-    lin_ms_launch = r["lin_ms"] / max(r["lin_launches"], 1)
-    lin_flops_launch = r["lin_flops"] / max(r["lin_launches"], 1)
+    # roofline of the TP GEMMs on rank 0 (the full-SM rank of every default plan);
+    # each rank's peak is its applied SM share x the sustained tensor peak
+    f0, ms0, n0, sh0 = r["lin_per_rank"][0]
+    lin_ms_launch = ms0 / max(n0, 1)
+    lin_flops_launch = f0 / max(n0, 1)
     achieved = lin_flops_launch / (lin_ms_launch / 1e3) / 1e12 if lin_ms_launch > 0 else None
+    peak0 = pk["bf16_tflops_sustained"] * sh0
+    per_rank_roof = [{"rank": i, "sm_share": round(sh, 4),
+                      "achieved_tflops": (fl / (ms / 1e3) / 1e12) if ms > 0 else None,
+                      "frac_of_share_peak": (fl / (ms / 1e3) / 1e12 / (pk["bf16_tflops_sustained"] * sh))
+                      if ms > 0 and sh > 0 else None}
+                     for i, (fl, ms, nl_, sh) in enumerate(r["lin_per_rank"])]
     traffic = None
     tf = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     if os.path.exists(tf):
@@ -396,21 +445,27 @@ def main():
                 "peak_per_rank": f"sm_share x {pk['bf16_tflops']} TFLOPS ({pk['source']})",
                 "aggregate_sm_share": s["aggregate_sm_share"]},
         "even_split": ev,
+        "even_split_other": evs[1:],
         "mfu_gap_vs_even": (ev["mfu_ref_convention"] - s["mfu_ref_convention"]) if ev else None,
         "e2e": {"value": s["e2e_tokens_per_s"], "unit": "tokens/s",
                 "h2d_bytes_per_step": int(r["h2d"]), "d2h_bytes_per_step": int(r["d2h"])},
         "gpu_launches": int(r["launches"] * a.steps),
         "roofline": {"bound": "tensor", "kernel": "tcgen05 TP GEMMs (QKV/O/gate-up/down, fwd+dgrad+wgrad)",
-                     "achieved": achieved, "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
-                     "frac": achieved / pk["bf16_tflops_sustained"] if achieved else None,
-                     "peak_kind": "sustained (kernel timed inside a long step)",
-                     "launches_per_step": r["lin_launches"] / max(
+                     "achieved": achieved, "peak": peak0, "unit": "TFLOP/s",
+                     "frac": achieved / peak0 if achieved else None,
+                     "peak_kind": "sustained (kernel timed inside a long step) x rank 0 SM share",
+                     "rank": 0, "per_rank": per_rank_roof,
+                     "timing": ("CUDA events captured around every GEMM in the step graph, "
+                                "last timed replay" if r.get("gemm_graph") else
+                                "CUDA events around every GEMM, eager profiled pass"),
+                     "launches_per_step": n0 / max(
                          r["stats"].get("gemm_profile", {}).get("steps", 1), 1),
                      "algorithmic_flops_per_launch": lin_flops_launch,
                      "avg_launch_ms": lin_ms_launch, "traffic": traffic},
-        "gemm_profile_rank0": r["stats"].get("gemm_profile"),
+        "gemm_profile_rank0": r.get("gemm_graph") or r["stats"].get("gemm_profile"),
         "phase_ms_rank0": r["stats"].get("ms"),
         "timeline_ms_rank0_profiled": r["stats"].get("timeline_ms"),
+        "timeline_ms_per_step_per_rank_profiled": r["tl_all"] if a.gpus > 1 else None,
         "sm_cap_rank0": {k: r["stats"].get(k) for k in ("sm_cap_mode", "sm_applied", "sm_total")},
         "clocks": r["clocks"],
         "cpu_baseline": cpu,

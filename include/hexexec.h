@@ -139,6 +139,10 @@ hexexec_status hexexec_k_gemm(int M, int N, int K, int nb1, int nb2, const void*
  * that many k-parts; ws (fp32, ws_bytes) and counters (n ints) must be zeroed
  * device memory, or NULL (then only beta GEMMs without workspace split). */
 hexexec_status hexexec_k_gemm_split(int split, float* ws, size_t ws_bytes, int* counters, int n);
+/* peer copies for later hexexec_k_gemm calls: every bf16 C tile is also
+ * TMA-stored to peers[k] (device pointers with C's layout, e.g. another GPU's
+ * buffer reachable over NVLink); n = 0 clears.  At most 3. */
+hexexec_status hexexec_k_gemm_peers(void* const* peers, int n);
 /* fused causal attention over the head-interleaved QKV buffer [mb*S, nh*3*d]:
  * out [mb*S, nh*d] bf16, lse [mb*nh, S] (log2 domain); backward writes
  * dq/dk/dv into dqkv [mb*S, nh*3*d] (delta / dq_acc: fp32 scratch of

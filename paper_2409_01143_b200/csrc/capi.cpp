@@ -289,6 +289,11 @@ struct KSplit {
   int n;
 };
 KSplit g_k_split = {-1, nullptr, 0, nullptr, 0};
+// peer copies of C for later hexexec_k_gemm calls (test / microbenchmark)
+struct KPeers {
+  void* p[hexexec::kMaxGemmPeers] = {nullptr, nullptr, nullptr};
+  int n = 0;
+} g_k_peers;
 }  // namespace
 
 hexexec_status hexexec_k_gemm(int M, int N, int K, int nb1, int nb2, const void* A, int a_mn,
@@ -317,7 +322,16 @@ hexexec_status hexexec_k_gemm(int M, int N, int K, int nb1, int nb2, const void*
   d.ws_bytes = g_k_split.ws_bytes;
   d.ws_cnt = g_k_split.cnt;
   d.ws_cnt_n = g_k_split.n;
+  d.npeer = g_k_peers.n;
+  for (int k = 0; k < g_k_peers.n; ++k) d.peer_C[k] = g_k_peers.p[k];
   return cuda_status(hexexec::gemm_bf16(d, as_stream(stream)));
+}
+
+hexexec_status hexexec_k_gemm_peers(void* const* peers, int n) {
+  if (n < 0 || n > hexexec::kMaxGemmPeers || (n > 0 && !peers)) return HEXEXEC_ERR_INVALID;
+  g_k_peers.n = n;
+  for (int k = 0; k < n; ++k) g_k_peers.p[k] = peers[k];
+  return HEXEXEC_OK;
 }
 
 hexexec_status hexexec_k_gemm_split(int split, float* ws, size_t ws_bytes, int* counters, int n) {

@@ -76,6 +76,9 @@ ExecConfig parse_exec_config(const std::string& text) {
       else if (k == "gemm_split") c.gemm_split = v.get<bool>();
       else if (k == "recompute") c.recompute = v.get<bool>();
       else if (k == "pp_protocol") c.pp_protocol = v.get<std::string>();
+      else if (k == "tp_reduce") c.tp_reduce = v.get<std::string>();
+      else if (k == "tp_direction") c.tp_direction = v.get<std::string>();
+      else if (k == "graph_gemm_events") c.graph_gemm_events = v.get<bool>();
       else throw ParseError("exec config: unknown key '" + k + "'");
     } catch (const nlohmann::json::exception& e) {
       throw ParseError("exec config: bad value for '" + k + "'");
@@ -89,6 +92,10 @@ ExecConfig parse_exec_config(const std::string& text) {
     throw ParseError("exec config: dp_comm_dtype must be bf16|fp32");
   if (c.pp_protocol != "direct" && c.pp_protocol != "leader")
     throw ParseError("exec config: pp_protocol must be direct|leader");
+  if (c.tp_reduce != "peer" && c.tp_reduce != "nccl")
+    throw ParseError("exec config: tp_reduce must be peer|nccl");
+  if (c.tp_direction != "auto" && c.tp_direction != "push")
+    throw ParseError("exec config: tp_direction must be auto|push");
   return c;
 }
 
@@ -206,6 +213,15 @@ class Executor {
   int32_t* tokens = nullptr;
   int32_t* tokens_pinned = nullptr;
   float* idle_loss_ = nullptr;
+  // TP exchange over peer memory (tp_reduce = "peer"): local buffer = 2 ring
+  // buffers x tp slots x [M, H] bf16 + flags[tp]; peers' buffers IPC-mapped
+  uint8_t* xbuf_ = nullptr;
+  uint8_t* xpeer_[4] = {nullptr, nullptr, nullptr, nullptr};
+  TpPeers tpp_{};
+  size_t xflag_off_ = 0;
+  unsigned xop_ = 0;
+  bool tp_peer_ = false;
+  int tp_crit_ = -1;  // TP index of the critical (slowest) rank, or -1
   float* recv_buf = nullptr;  // fwd activations received (fp32 [M,H]) go into slot x[0]
   int64_t step_index = 0;
   // stats
@@ -236,6 +252,10 @@ class Executor {
     if (world_comm) ncclCommDestroy(world_comm);
     world_comm = nullptr;
     arena.release();
+    for (auto& p : xpeer_)
+      if (p) cudaIpcCloseMemHandle(p), p = nullptr;
+    if (xbuf_) cudaFree(xbuf_);
+    xbuf_ = nullptr;
     if (idle_loss_) cudaFree(idle_loss_);
     idle_loss_ = nullptr;
     if (tokens_pinned) cudaFreeHost(tokens_pinned);
@@ -255,6 +275,12 @@ class Executor {
     gemm_pool_.clear();
     for (auto& e : mark_pool_) cudaEventDestroy(e);
     mark_pool_.clear();
+    for (auto& r : graph_recs_) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    graph_recs_.clear();
+    graph_shapes_.clear();
     if (gexec_) cudaGraphExecDestroy(gexec_);
     gexec_ = nullptr;
     for (auto& g : groups_)
@@ -317,6 +343,7 @@ class Executor {
     setup_comms(uid, uid_len);
     if (role.active) {
       allocate();
+      setup_tp_exchange();
       init_params();
       build_groups();
       if (!cstream) cfg.dp_overlap = false;
@@ -474,9 +501,10 @@ class Executor {
     // memory tier: the device's memory_gib caps the rank (cost_model.cpp:130-153
     // applies the same per-device budget to its layer-memory estimate)
     const double cap = L.cluster.devices[size_t(role.device)].memory_gib * double(1ull << 30);
-    if (double(arena.total()) > cap)
+    if (double(arena.total() + tp_exchange_bytes()) > cap)
       throw Infeasible("plan does not fit device '" + L.cluster.devices[size_t(role.device)].id +
-                       "': rank needs " + std::to_string(arena.total() >> 20) + " MiB, memory_gib " +
+                       "': rank needs " + std::to_string((arena.total() + tp_exchange_bytes()) >> 20) +
+                       " MiB, memory_gib " +
                        std::to_string(L.cluster.devices[size_t(role.device)].memory_gib));
     if (cfg.validate_only) return;
     arena.commit();
@@ -652,6 +680,31 @@ class Executor {
   double gemm_ms_[3] = {0, 0, 0}, gemm_flops_[3] = {0, 0, 0};
   int64_t gemm_count_[3] = {0, 0, 0};
 
+  // graph_gemm_events: the same event pairs captured into the step graph, so
+  // every replay (the bench's timed region) re-times each GEMM in place; read
+  // after a sync from the last replay
+  // (only the GEMMs of one micro-batch, n_mb / 2, are bracketed: ~2 us per
+  // event node would otherwise add ~3% to the step)
+  std::vector<GemmRec> graph_recs_;
+  std::vector<std::string> graph_shapes_;
+  bool capturing_ = false;
+  int64_t cur_mb_ = 0;
+  double ggemm_ms_[3] = {0, 0, 0}, ggemm_flops_[3] = {0, 0, 0};
+  int64_t ggemm_count_[3] = {0, 0, 0};
+  void collect_graph_gemm() {
+    if (!gexec_ || graph_recs_.empty()) return;
+    for (int k = 0; k < 3; ++k) ggemm_ms_[k] = ggemm_flops_[k] = 0, ggemm_count_[k] = 0;
+    for (const auto& r : graph_recs_) {
+      float ms = 0;
+      if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+        ggemm_ms_[r.kind] += ms;
+        ggemm_flops_[r.kind] += r.flops;
+        ggemm_count_[r.kind] += 1;
+      }
+    }
+    (void)cudaGetLastError();
+  }
+
   void gemm(const GemmDesc& gin) {
     GemmDesc g = gin;
     g.split = cfg.gemm_split ? -1 : 0;
@@ -671,11 +724,26 @@ class Executor {
       double full = 2.0 * g.M * double(g.N) * g.K * g.nb1 * g.nb2;
       rec->flops = g.causal != kCausalNone ? full * (double(g.M) + 1) / (2.0 * g.M) : full;
       rec->kind = gemm_kind_;
-      HX_CUDA(cudaEventRecord(rec->a, stream));
+      HX_CUDA(cudaEventRecordWithFlags(rec->a, stream, capturing_ ? cudaEventRecordExternal : 0));
+    } else if (capturing_ && cfg.graph_gemm_events && cur_mb_ == role.n_mb / 2) {
+      GemmRec r{};
+      HX_CUDA(cudaEventCreate(&r.a));
+      HX_CUDA(cudaEventCreate(&r.b));
+      double full = 2.0 * g.M * double(g.N) * g.K * g.nb1 * g.nb2;
+      r.flops = g.causal != kCausalNone ? full * (double(g.M) + 1) / (2.0 * g.M) : full;
+      r.kind = gemm_kind_;
+      graph_recs_.push_back(r);
+      graph_shapes_.push_back(std::to_string(g.M) + "x" + std::to_string(g.N) + "x" +
+                              std::to_string(g.K) + (g.A.mn_major ? " A:mn" : " A:k") +
+                              (g.B.mn_major ? " B:mn" : " B:k") + (g.beta ? " beta" : "") +
+                              (g.npeer ? " peer" + std::to_string(g.npeer) : "") +
+                              (g.nb1 * g.nb2 > 1 ? " batch" + std::to_string(g.nb1 * g.nb2) : ""));
+      rec = &graph_recs_.back();
+      HX_CUDA(cudaEventRecordWithFlags(rec->a, stream, capturing_ ? cudaEventRecordExternal : 0));
     }
     cudaError_t e = gemm_bf16(g, stream);
     if (e != cudaSuccess) throw CudaError(std::string("gemm: ") + cudaGetErrorString(e));
-    if (rec) HX_CUDA(cudaEventRecord(rec->b, stream));
+    if (rec) HX_CUDA(cudaEventRecordWithFlags(rec->b, stream, capturing_ ? cudaEventRecordExternal : 0));
     ++launches_step;
     mark(gemm_kind_ == 0 ? "gemm_linear" : gemm_kind_ == 1 ? "gemm_attention" : "gemm_lm_head");
   }
@@ -730,6 +798,113 @@ class Executor {
 
   int32_t* tok_of(int64_t mbi) { return tokens + mbi * mb * (S + 1); }
 
+  // ------------------------------------------------------------ TP exchange
+  bool use_tp_peer() const { return role.tp > 1 && cfg.tp_reduce == "peer"; }
+  size_t tp_slot_elems() const { return size_t(M * H); }
+  size_t tp_exchange_bytes() const {
+    if (!use_tp_peer()) return 0;
+    return 2 * size_t(role.tp) * tp_slot_elems() * 2 + 256;
+  }
+
+  // exchange buffers: allocate, export (cudaIpc), all-gather the handles over
+  // the TP communicator, map every peer's buffer
+  void setup_tp_exchange() {
+    if (!use_tp_peer()) return;
+    if (role.tp > 4) throw LimitExceeded("tp_reduce=peer supports tp <= 4");
+    ncclComm_t c = tp_comm();
+    int me = 0, n = 0;
+    HX_NCCL(ncclCommUserRank(c, &me));
+    HX_NCCL(ncclCommCount(c, &n));
+    if (n != role.tp) throw CudaError("TP communicator size mismatch");
+    xflag_off_ = 2 * size_t(role.tp) * tp_slot_elems() * 2;
+    HX_CUDA(cudaMalloc(&xbuf_, tp_exchange_bytes()));
+    HX_CUDA(cudaMemset(xbuf_ + xflag_off_, 0, 256));
+    cudaIpcMemHandle_t h;
+    HX_CUDA(cudaIpcGetMemHandle(&h, xbuf_));
+    // one record per rank: IPC handle + the SM count actually applied
+    struct Rec {
+      cudaIpcMemHandle_t h;
+      int sms;
+      int pad[15];
+    };
+    Rec mine{};
+    mine.h = h;
+    mine.sms = sm_applied;
+    const size_t hs = sizeof(Rec);
+    char* dh = nullptr;
+    HX_CUDA(cudaMalloc(&dh, hs * size_t(n)));
+    HX_CUDA(cudaMemcpy(dh + hs * size_t(me), &mine, hs, cudaMemcpyHostToDevice));
+    HX_NCCL(ncclAllGather(dh + hs * size_t(me), dh, hs, ncclChar, c, stream));
+    std::vector<Rec> all(static_cast<size_t>(n));
+    HX_CUDA(cudaMemcpyAsync(all.data(), dh, hs * size_t(n), cudaMemcpyDeviceToHost, stream));
+    HX_CUDA(cudaStreamSynchronize(stream));
+    cudaFree(dh);
+    tpp_ = TpPeers{};
+    tpp_.tp = n;
+    tpp_.me = me;
+    tpp_.local = reinterpret_cast<unsigned long long*>(xbuf_ + xflag_off_);
+    for (int k = 0; k < n; ++k) {
+      if (k == me) continue;
+      void* p = nullptr;
+      HX_CUDA(cudaIpcOpenMemHandle(&p, all[size_t(k)].h, cudaIpcMemLazyEnablePeerAccess));
+      xpeer_[k] = static_cast<uint8_t*>(p);
+      tpp_.remote[k] = reinterpret_cast<unsigned long long*>(xpeer_[k] + xflag_off_) + me;
+    }
+    tp_peer_ = true;
+    // Asymmetric direction: the rank with the largest work / SM share (the
+    // step's critical path) stores its partial only locally -- the NVLink
+    // tail of a peer store would extend its GEMMs -- and the faster ranks,
+    // which wait for it anyway, pull it with a copy-engine transfer.  Even
+    // stages (no rank >= 5% slower than the next) push symmetrically.
+    std::vector<double> ratio;
+    for (int k = 0; k < n; ++k) {
+      // comm rank k = position in the sorted TP rank set (setup_comms' key)
+      const RankRole& q = L.roles[size_t(L.comm_sets[size_t(L.tp_comm[size_t(rank)])][size_t(k)])];
+      const double work = double(q.heads.size()) * 4.0 * double(d) * double(H) +
+                          double(q.ffn_chunks.size()) * 64.0 * 3.0 * double(H);
+      const double share = double(std::max(all[size_t(k)].sms, 1)) / double(std::max(sm_total, 1));
+      ratio.push_back(work / share);
+    }
+    const int crit = int(std::max_element(ratio.begin(), ratio.end()) - ratio.begin());
+    double second = 0;
+    for (int k = 0; k < n; ++k)
+      if (k != crit) second = std::max(second, ratio[size_t(k)]);
+    tp_crit_ = ratio[size_t(crit)] >= 1.05 * second ? crit : -1;
+    if (cfg.tp_direction == "push") tp_crit_ = -1;
+  }
+
+  // slot `src` of ring buffer `b` on TP rank `owner` (owner == me: local)
+  bf16* xslot(int owner, unsigned b, int src) {
+    uint8_t* base = owner == tpp_.me ? xbuf_ : xpeer_[owner];
+    return reinterpret_cast<bf16*>(base) + (size_t(b) * size_t(role.tp) + size_t(src)) * tp_slot_elems();
+  }
+
+  // row-parallel partial GEMM: C goes to this rank's slot of the current ring
+  // buffer locally and on every peer.  Returns the buffer's slot 0; the
+  // consumer sums tp slots (tp_slot_elems apart) after tp_sync().
+  const bf16* tp_partial_gemm(GemmDesc g) {
+    const unsigned b = xop_ & 1u;
+    g.C = xslot(tpp_.me, b, tpp_.me);
+    g.npeer = 0;
+    if (tpp_.me != tp_crit_)
+      for (int k = 0; k < role.tp; ++k)
+        if (k != tpp_.me) g.peer_C[g.npeer++] = xslot(k, b, tpp_.me);
+    gemm(g);
+    return xslot(tpp_.me, b, 0);
+  }
+  void tp_sync() {
+    if (xop_ >= (1u << 24)) throw LimitExceeded("too many TP exchanges per step");
+    const unsigned b = xop_ & 1u;
+    k_tp_sync(tpp_, sp_, xop_++, stream);
+    kcheck("tp_sync");
+    if (tp_crit_ >= 0 && tpp_.me != tp_crit_ && !pad_) {
+      HX_CUDA(cudaMemcpyAsync(xslot(tpp_.me, b, tp_crit_), xslot(tp_crit_, b, tp_crit_),
+                              tp_slot_elems() * 2, cudaMemcpyDeviceToDevice, stream));
+      mark("tp_pull");
+    }
+  }
+  bool pad_ = false;
+
   // ------------------------------------------------------------ forward
   LayerActs& acts(Slot& sl, int64_t l) { return cfg.recompute ? rc_acts_ : sl.layers[size_t(l)]; }
 
@@ -754,6 +929,12 @@ class Executor {
       gemm(g);
       k_rmsnorm_fwd(a.x_mid, nullptr, nullptr, w.mlp_norm.p32, a.hn, a.rstd2, int(M), int(H), eps, stream);
       kcheck("rmsnorm_fwd");
+    } else if (tp_peer_) {
+      const bf16* y = tp_partial_gemm(g2(M, H, kr, a.attn, 0, kr, w.wo.p16, 1, H, nullptr, H, 0));
+      tp_sync();
+      k_rmsnorm_fwd(x_in, y, a.x_mid, w.mlp_norm.p32, a.hn, a.rstd2, int(M), int(H), eps, stream,
+                    role.tp, int64_t(tp_slot_elems()));
+      kcheck("rmsnorm_fwd");
     } else {
       gemm(g2(M, H, kr, a.attn, 0, kr, w.wo.p16, 1, H, ypart, H, 0));
       tp_allreduce_bf16(ypart, M * H);
@@ -769,6 +950,11 @@ class Executor {
       GemmDesc g = g2(M, H, F, a.act, 0, F, w.wdown.p16, 1, H, x_out, H, 1);
       g.R = a.x_mid;
       gemm(g);
+    } else if (tp_peer_) {
+      const bf16* y = tp_partial_gemm(g2(M, H, F, a.act, 0, F, w.wdown.p16, 1, H, nullptr, H, 0));
+      tp_sync();
+      k_residual_add(a.x_mid, y, x_out, M * H, stream, role.tp, int64_t(tp_slot_elems()));
+      kcheck("residual_add");
     } else {
       gemm(g2(M, H, F, a.act, 0, F, w.wdown.p16, 1, H, ypart, H, 0));
       tp_allreduce_bf16(ypart, M * H);
@@ -861,6 +1047,7 @@ class Executor {
   }
 
   void forward(int64_t mbi, Slot& sl) {
+    cur_mb_ = mbi;
     if (role.first_stage) {
       k_embed_fwd(tok_of(mbi), embed.p32, sl.x[0], int(M), int(S), int(H), stream);
       kcheck("embed_fwd");
@@ -885,18 +1072,27 @@ class Executor {
     }
     k_swiglu_bwd(a.gu, da, dgu, int(M), int(F), stream);
     kcheck("swiglu_bwd");
-    gemm(g2(M, H, 2 * F, dgu, 0, 2 * F, w.wgu.p16, 1, H, dy16, H, 0));
+    const bf16* dyr = dy16;
+    if (tp_peer_)
+      dyr = tp_partial_gemm(g2(M, H, 2 * F, dgu, 0, 2 * F, w.wgu.p16, 1, H, nullptr, H, 0));
+    else
+      gemm(g2(M, H, 2 * F, dgu, 0, 2 * F, w.wgu.p16, 1, H, dy16, H, 0));
     {
       GemmDesc g = g2(2 * F, H, M, dgu, 1, 2 * F, a.hn, 1, H, w.wgu.g32, H, 1);
       g.beta = first_mb ? 0 : 1;
       gemm(g);
     }
-    tp_allreduce_bf16(dy16, M * H);
+    if (tp_peer_)
+      tp_sync();
+    else
+      tp_allreduce_bf16(dy16, M * H);
+    const int ny = tp_peer_ ? int(role.tp) : 1;
+    const int64_t ys = int64_t(tp_slot_elems());
     // dx_mid = dx_out + rmsnorm_bwd(dhn);  (reuse dxi as dx_mid storage)
     float* dxm = dxi;
     bf16* dxmb = dxib;
-    k_rmsnorm_bwd(dy16, nullptr, a.x_mid, a.rstd2, w.mlp_norm.p32, dxo, dxm, dxmb, w.mlp_norm.g32,
-                  int(M), int(H), dg_part_, stream);
+    k_rmsnorm_bwd(dyr, nullptr, a.x_mid, a.rstd2, w.mlp_norm.p32, dxo, dxm, dxmb, w.mlp_norm.g32,
+                  int(M), int(H), dg_part_, stream, ny, ys);
     kcheck("rmsnorm_bwd");
     // attention: O projection
     gemm(g2(M, kr, H, dxmb, 0, H, w.wo.p16, 0, H, dattn, kr, 0));
@@ -908,16 +1104,22 @@ class Executor {
     attention_bwd(a);
     k_rope(dqkv, int(M), int(S), int(nh), int(d), float(L.model.rope_theta), 1, stream);
     kcheck("rope");
-    gemm(g2(M, H, qkvw, dqkv, 0, qkvw, w.wqkv.p16, 1, H, dy16, H, 0));
+    if (tp_peer_)
+      dyr = tp_partial_gemm(g2(M, H, qkvw, dqkv, 0, qkvw, w.wqkv.p16, 1, H, nullptr, H, 0));
+    else
+      gemm(g2(M, H, qkvw, dqkv, 0, qkvw, w.wqkv.p16, 1, H, dy16, H, 0));
     {
       GemmDesc g = g2(qkvw, H, M, dqkv, 1, qkvw, a.xn, 1, H, w.wqkv.g32, H, 1);
       g.beta = first_mb ? 0 : 1;
       gemm(g);
     }
-    tp_allreduce_bf16(dy16, M * H);
+    if (tp_peer_)
+      tp_sync();
+    else
+      tp_allreduce_bf16(dy16, M * H);
     // dx_in = dx_mid + rmsnorm_bwd(dxn): in place over dx_mid (row-local)
-    k_rmsnorm_bwd(dy16, nullptr, sl.x[size_t(l)], a.rstd1, w.attn_norm.p32, dxm, dxi, dxib,
-                  w.attn_norm.g32, int(M), int(H), dg_part_, stream);
+    k_rmsnorm_bwd(dyr, nullptr, sl.x[size_t(l)], a.rstd1, w.attn_norm.p32, dxm, dxi, dxib,
+                  w.attn_norm.g32, int(M), int(H), dg_part_, stream, ny, ys);
     kcheck("rmsnorm_bwd");
   }
 
@@ -997,19 +1199,28 @@ class Executor {
   // backward of one micro-batch; dx_top (fp32) is the grad of the stage output
   // (received), or null on the last stage (starts from dlogits)
   void backward(int64_t mbi, Slot& sl, float* dx_top) {
+    cur_mb_ = mbi;
     float* cur = dx[0];
     float* nxt = dx[1];
     bf16* curb = dxb;
     if (role.last_stage) {
       gemm_kind_ = 2;
-      gemm(g2(M, H, Vr, sl.dlogits, 0, Vr, lm_head.p16, 1, H, dy16, H, 0));
+      const bf16* dyr = dy16;
+      if (tp_peer_)
+        dyr = tp_partial_gemm(g2(M, H, Vr, sl.dlogits, 0, Vr, lm_head.p16, 1, H, nullptr, H, 0));
+      else
+        gemm(g2(M, H, Vr, sl.dlogits, 0, Vr, lm_head.p16, 1, H, dy16, H, 0));
       GemmDesc g = g2(Vr, H, M, sl.dlogits, 1, Vr, sl.xf, 1, H, lm_head.g32, H, 1);
       g.beta = accum_first_ ? 0 : 1;
       gemm(g);
       gemm_kind_ = 0;
-      tp_allreduce_bf16(dy16, M * H);
-      k_rmsnorm_bwd(dy16, nullptr, sl.x[size_t(nl)], sl.rstdf, final_norm.p32, nullptr, cur, curb,
-                    final_norm.g32, int(M), int(H), dg_part_, stream);
+      if (tp_peer_)
+        tp_sync();
+      else
+        tp_allreduce_bf16(dy16, M * H);
+      k_rmsnorm_bwd(dyr, nullptr, sl.x[size_t(nl)], sl.rstdf, final_norm.p32, nullptr, cur, curb,
+                    final_norm.g32, int(M), int(H), dg_part_, stream, tp_peer_ ? int(role.tp) : 1,
+                    int64_t(tp_slot_elems()));
       kcheck("rmsnorm_bwd");
       group_ready(kGroupHead);
     } else {
@@ -1218,7 +1429,7 @@ class Executor {
 
   void dp_sync_and_update() {
     const auto& buckets = L.dp_buckets[size_t(rank)];
-    cudaEventRecord(ev[2], stream);
+    cudaEventRecordWithFlags(ev[2], stream, capturing_ ? cudaEventRecordExternal : 0);
     const bool bf = G16 != nullptr;
     // 1. weight by samples: scale = (batch_i / global_batch) / multiplicity, fused
     //    with the bf16 cast for tensors that take part in a DP allreduce
@@ -1247,7 +1458,7 @@ class Executor {
       HX_NCCL(ncclGroupEnd());
       mark("nccl_dp_allreduce");
     }
-    cudaEventRecord(ev[3], stream);
+    cudaEventRecordWithFlags(ev[3], stream, capturing_ ? cudaEventRecordExternal : 0);
     // 3. AdamW per tensor (weight decay only on matrices)
     const float t = float(step_index + 1);
     const float bc1 = 1.f - std::pow(cfg.beta1, t);
@@ -1264,7 +1475,7 @@ class Executor {
               gscale, cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, wd, bc1, bc2, stream, sp_);
       kcheck("adamw");
     }
-    cudaEventRecord(ev[4], stream);
+    cudaEventRecordWithFlags(ev[4], stream, capturing_ ? cudaEventRecordExternal : 0);
   }
 
   // is [off, off+cnt) fully covered by this rank's DP buckets? (buckets never
@@ -1307,13 +1518,16 @@ class Executor {
       ev = ev_graph_;  // the graph owns its own phase events
       HX_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeRelaxed));
       cudaGraph_t g = nullptr;
+      capturing_ = true;
       try {
         enqueue_body();
       } catch (...) {
+        capturing_ = false;
         cudaStreamEndCapture(stream, &g);
         if (g) cudaGraphDestroy(g);
         throw;
       }
+      capturing_ = false;
       HX_CUDA(cudaStreamEndCapture(stream, &g));
       cudaError_t e = cudaGraphInstantiate(&gexec_, g, 0);
       cudaGraphDestroy(g);
@@ -1330,8 +1544,9 @@ class Executor {
 
   void enqueue_body() {
     launches_step = 0;
+    xop_ = 0;
     nccl_calls_step = 0;
-    cudaEventRecord(ev[0], stream);
+    cudaEventRecordWithFlags(ev[0], stream, capturing_ ? cudaEventRecordExternal : 0);
     k_step_tick(sp_, cfg.beta1, cfg.beta2, stream);
     kcheck("step_tick");
     if (role.first_stage || role.last_stage) {
@@ -1347,24 +1562,31 @@ class Executor {
         HX_CUDA(cudaMemsetAsync(G32 + rt.offset, 0, size_t(rt.rows * ts.cols) * 4, stream));
     }
     mark("prologue");
-    cudaEventRecord(ev[1], stream);
+    cudaEventRecordWithFlags(ev[1], stream, capturing_ ? cudaEventRecordExternal : 0);
     if (cfg.dp_overlap) {
       // fork the comm stream into this step (and into the graph when capturing)
       HX_CUDA(cudaEventRecord(join_ev_, stream));
       HX_CUDA(cudaStreamWaitEvent(cstream, join_ev_, 0));
     }
     run_pipeline();
+    // even number of exchanges per step: ring buffer b = op & 1 alternates
+    // across the step boundary too (the double-buffer hand-off argument)
+    if (tp_peer_ && (xop_ & 1u)) {
+      pad_ = true;
+      tp_sync();
+      pad_ = false;
+    }
     if (cfg.dp_overlap) {
       HX_CUDA(cudaEventRecord(join_ev_, cstream));
       HX_CUDA(cudaStreamWaitEvent(stream, join_ev_, 0));
-      cudaEventRecord(ev[2], stream);
-      cudaEventRecord(ev[3], stream);
-      cudaEventRecord(ev[4], stream);
+      cudaEventRecordWithFlags(ev[2], stream, capturing_ ? cudaEventRecordExternal : 0);
+      cudaEventRecordWithFlags(ev[3], stream, capturing_ ? cudaEventRecordExternal : 0);
+      cudaEventRecordWithFlags(ev[4], stream, capturing_ ? cudaEventRecordExternal : 0);
     } else {
       dp_sync_and_update();
     }
     finish_loss();
-    cudaEventRecord(ev[5], stream);
+    cudaEventRecordWithFlags(ev[5], stream, capturing_ ? cudaEventRecordExternal : 0);
   }
 
   void finish_loss() {
@@ -1395,6 +1617,7 @@ class Executor {
     if (role.active) collect_times();
     steps_since_collect_ = 1;
     collect_gemm_profile();
+    collect_graph_gemm();
     collect_timeline();
     if (loss_out) *loss_out = last_loss;
   }
@@ -1416,6 +1639,7 @@ class Executor {
     j["sm_total"] = sm_total;
     j["sm_applied"] = sm_applied;
     j["sm_cap_mode"] = sm_mode;
+    j["tp_reduce"] = tp_peer_ ? (tp_crit_ >= 0 ? "peer(pull from tp rank " + std::to_string(tp_crit_) + ")" : std::string("peer(push)")) : (role.tp > 1 ? std::string("nccl") : std::string("none"));
     j["sm_fraction"] = role.sm_fraction;
     j["arena_bytes"] = arena.total();
     j["activation_slots"] = n_slots;
@@ -1439,6 +1663,34 @@ class Executor {
       ojson tl;
       for (const auto& [k, v] : timeline_) tl[k] = {{"ms", v.first}, {"ops", v.second}};
       j["timeline_ms"] = tl;
+    }
+    if (!graph_recs_.empty()) {
+      const char* names[3] = {"tp_linear", "attention", "lm_head"};
+      ojson g;
+      for (int k = 0; k < 3; ++k)
+        g[names[k]] = {{"launches", ggemm_count_[k]}, {"ms", ggemm_ms_[k]},
+                       {"flops", ggemm_flops_[k]},
+                       {"tflops", ggemm_ms_[k] > 0 ? ggemm_flops_[k] / ggemm_ms_[k] / 1e9 : 0.0}};
+      g["steps"] = 1;
+      g["micro_batches_sampled"] = 1;
+      g["micro_batches"] = role.n_mb;
+      g["source"] = "CUDA events captured in the step graph around micro-batch n_mb/2's GEMMs, last replay";
+      std::map<std::string, std::tuple<double, double, int64_t>> by;
+      for (size_t i = 0; i < graph_recs_.size(); ++i) {
+        float ms = 0;
+        if (cudaEventElapsedTime(&ms, graph_recs_[i].a, graph_recs_[i].b) != cudaSuccess) continue;
+        auto& t = by[graph_shapes_[i]];
+        std::get<0>(t) += ms;
+        std::get<1>(t) += graph_recs_[i].flops;
+        std::get<2>(t) += 1;
+      }
+      (void)cudaGetLastError();
+      ojson sh = ojson::array();
+      for (const auto& [k, v] : by)
+        sh.push_back({{"shape", k}, {"launches", std::get<2>(v)}, {"ms", std::get<0>(v)},
+                      {"tflops", std::get<0>(v) > 0 ? std::get<1>(v) / std::get<0>(v) / 1e9 : 0.0}});
+      g["shapes"] = sh;
+      j["gemm_profile_graph"] = g;
     }
     return j.dump();
   }
@@ -1491,6 +1743,7 @@ void executor_sync(Executor& e) {
   e.last_loss = e.loss_host[0] / float(e.L.plan.global_batch * e.S);
   if (e.role.active) e.collect_times();
   e.collect_gemm_profile();
+  e.collect_graph_gemm();
   e.collect_timeline();
 }
 

@@ -18,6 +18,7 @@ struct ExecConfig {
   std::string dp_comm_dtype = "bf16"; // "bf16" | "fp32"
   bool validate_only = false;
   bool profile_gemm = false;          // per-GEMM CUDA events (roofline evidence); eager
+  bool graph_gemm_events = false;     // per-GEMM CUDA events inside the step graph
   bool cuda_graph = true;             // replay the captured step graph (after step 0)
   std::string attention = "fused";    // "fused" (flash, tcgen05) | "unfused" (GEMM+softmax)
   bool dp_overlap = true;             // DP sync + AdamW per layer on a second stream
@@ -34,6 +35,14 @@ struct ExecConfig {
   // stages' first devices exchange it and the receiving leader broadcasts it
   // over its TP communicator (for links where only leaders are well connected)
   std::string pp_protocol = "direct";
+  // TP reduction of the row-parallel partials: "peer" = the producing GEMM's
+  // epilogue TMA-stores its partial into every TP peer's exchange buffer
+  // (IPC-mapped, NVLink) while it runs, a flag handshake orders it, and the
+  // consumer (RMSNorm / residual add) sums the slots; "nccl" = ncclAllReduce
+  std::string tp_reduce = "peer";
+  // "auto": the critical rank of an uneven TP stage does not push (the others
+  // pull its partial); "push": every rank pushes
+  std::string tp_direction = "auto";
 };
 
 ExecConfig parse_exec_config(const std::string& text);

@@ -31,6 +31,8 @@ enum GemmCausal : int {
   kCausalKUpper = 3,     // k range limited to [m0, K)                  (A^T of lower-tri)
 };
 
+constexpr int kMaxGemmPeers = 3;
+
 struct GemmDesc {
   int M = 0, N = 0, K = 0;
   int nb1 = 1, nb2 = 1;
@@ -53,6 +55,11 @@ struct GemmDesc {
   int* ws_cnt = nullptr;
   int ws_cnt_n = 0;
   int split = -1;
+  // TP peer copies: every C tile is also TMA-stored to peer_C[k] (same layout,
+  // bf16, no beta / split; typically IPC-mapped buffers of the other TP ranks
+  // so the row-parallel partials cross NVLink while the GEMM still runs)
+  void* peer_C[kMaxGemmPeers] = {nullptr, nullptr, nullptr};
+  int npeer = 0;
 };
 
 // workspace a GemmDesc needs for any split (bytes, counters)

@@ -47,6 +47,13 @@ struct EpiParams {
   int split_direct;  // partials reduce-add straight into C (beta, no R)
   float* ws;         // [split tiles][TM][BN] fp32
   int* ws_cnt;       // per (split tile, 32-row slab)
+  int npeer;         // extra copies of every stored C tile (TP peers' buffers)
+};
+
+// TMA maps of the peer copies of C (IPC-mapped buffers of the other TP ranks,
+// reached over NVLink): the epilogue stores each tile to C and to every peer
+struct alignas(64) PeerMaps {
+  CUtensorMap m[kMaxGemmPeers];
 };
 
 template <int BN, int CG>
@@ -157,7 +164,8 @@ template <int BN, int A_MN, int B_MN, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmR,
-                const __grid_constant__ CUtensorMap tmW, const EpiParams p) {
+                const __grid_constant__ CUtensorMap tmW, const __grid_constant__ PeerMaps pm,
+                const EpiParams p) {
   using C = Cfg<BN, CG>;
   constexpr int ST = C::STAGES;
   constexpr int TM = C::TM;
@@ -398,8 +406,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_reduce_add_4d(&tmW, sbuf, c, wrow, 0, 0);
             else if (p.beta || split)
               tma_reduce_add_4d(&tmC, sbuf, col, row0, z1, z2);
-            else
+            else {
               tma_store_4d(&tmC, sbuf, col, row0, z1, z2);
+              for (int k = 0; k < p.npeer; ++k) tma_store_4d(&pm.m[k], sbuf, col, row0, z1, z2);
+            }
             bulk_commit();
           }
           sb ^= 1;
@@ -501,7 +511,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    if (lane == 0) bulk_wait_all();
+    if (lane == 0) {
+      bulk_wait_all();
+      if (p.npeer) {  // peer copies complete and visible before the kernel ends
+        fence_proxy_async_global();
+        __threadfence_system();
+      }
+    }
   }
 
   tc_fence_before();
@@ -585,8 +601,8 @@ bool make_map_c(CUtensorMap* map, void* ptr, int fp32, long long N, long long M,
 
 template <int BN, int AM, int BMn, int CG>
 cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
-                     const CUtensorMap& mr, const CUtensorMap& mw, EpiParams p, int grid,
-                     cudaStream_t s) {
+                     const CUtensorMap& mr, const CUtensorMap& mw, const PeerMaps& pm,
+                     EpiParams p, int grid, cudaStream_t s) {
   using C = Cfg<BN, CG>;
   static bool attr_done = false;
   auto kern = gemm_kernel<BN, AM, BMn, CG>;
@@ -609,17 +625,17 @@ cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mr, mw, p);
+  return cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mr, mw, pm, p);
 }
 
 template <int BN, int CG>
 cudaError_t dispatch_major(int am, int bm, const CUtensorMap& ma, const CUtensorMap& mb,
                            const CUtensorMap& mc, const CUtensorMap& mr, const CUtensorMap& mw,
-                           const EpiParams& p, int grid, cudaStream_t s) {
-  if (!am && !bm) return launch_t<BN, 0, 0, CG>(ma, mb, mc, mr, mw, p, grid, s);
-  if (!am && bm) return launch_t<BN, 0, 1, CG>(ma, mb, mc, mr, mw, p, grid, s);
-  if (am && !bm) return launch_t<BN, 1, 0, CG>(ma, mb, mc, mr, mw, p, grid, s);
-  return launch_t<BN, 1, 1, CG>(ma, mb, mc, mr, mw, p, grid, s);
+                           const PeerMaps& pm, const EpiParams& p, int grid, cudaStream_t s) {
+  if (!am && !bm) return launch_t<BN, 0, 0, CG>(ma, mb, mc, mr, mw, pm, p, grid, s);
+  if (!am && bm) return launch_t<BN, 0, 1, CG>(ma, mb, mc, mr, mw, pm, p, grid, s);
+  if (am && !bm) return launch_t<BN, 1, 0, CG>(ma, mb, mc, mr, mw, pm, p, grid, s);
+  return launch_t<BN, 1, 1, CG>(ma, mb, mc, mr, mw, pm, p, grid, s);
 }
 
 // Split of the tail wave: T tiles on P pairs run q = T / P full rounds and a
@@ -703,6 +719,15 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream) {
   } else {
     mr = mc;
   }
+  static_assert(sizeof(PeerMaps) == kMaxGemmPeers * sizeof(CUtensorMap), "PeerMaps layout");
+  PeerMaps pm;
+  p.npeer = d.npeer;
+  if (d.npeer < 0 || d.npeer > kMaxGemmPeers) return cudaErrorInvalidValue;
+  if (d.npeer && (d.beta || d.c_fp32)) return cudaErrorInvalidValue;
+  for (int k = 0; k < d.npeer; ++k)
+    if (!make_map_c(&pm.m[k], d.peer_C[k], 0, d.N, d.M, d.ldc, d.cbs1, d.cbs2, d.nb1, d.nb2))
+      return cudaErrorInvalidValue;
+  for (int k = d.npeer; k < kMaxGemmPeers; ++k) pm.m[k] = mc;
   const int sms = g_sm_limit > 0 ? std::min(g_sm_limit, g_num_sms) : g_num_sms;
   const int P = std::max(1, sms / CG);
   // tail split (dense GEMMs only)
@@ -713,7 +738,7 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream) {
   p.ws = d.ws;
   p.ws_cnt = d.ws_cnt;
   CUtensorMap mw = mc;
-  if (d.causal == kCausalNone && d.split != 0 && p.num_tiles > 0) {
+  if (d.causal == kCausalNone && d.split != 0 && d.npeer == 0 && p.num_tiles > 0) {
     const int kblocks = (d.K + BK - 1) / BK;
     const bool direct = d.beta && !d.R;
     int s = d.split > 1 ? std::min(d.split, std::max(1, kblocks))
@@ -733,11 +758,11 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream) {
   const int grid = std::min(p.num_units, P) * CG;
   const int am = d.A.mn_major, bmj = d.B.mn_major;
   if (CG == 2) {
-    if (BN == 256) return dispatch_major<256, 2>(am, bmj, ma, mb, mc, mr, mw, p, grid, stream);
-    return dispatch_major<128, 2>(am, bmj, ma, mb, mc, mr, mw, p, grid, stream);
+    if (BN == 256) return dispatch_major<256, 2>(am, bmj, ma, mb, mc, mr, mw, pm, p, grid, stream);
+    return dispatch_major<128, 2>(am, bmj, ma, mb, mc, mr, mw, pm, p, grid, stream);
   }
-  if (BN == 256) return dispatch_major<256, 1>(am, bmj, ma, mb, mc, mr, mw, p, grid, stream);
-  return dispatch_major<128, 1>(am, bmj, ma, mb, mc, mr, mw, p, grid, stream);
+  if (BN == 256) return dispatch_major<256, 1>(am, bmj, ma, mb, mc, mr, mw, pm, p, grid, stream);
+  return dispatch_major<128, 1>(am, bmj, ma, mb, mc, mr, mw, pm, p, grid, stream);
 }
 
 }  // namespace hexexec

@@ -178,7 +178,7 @@ template <int NC>
 __global__ void __launch_bounds__(kNormThreads)
     rmsnorm_fwd_kernel(const float* __restrict__ x, const bf16* __restrict__ y, float* xo,
                        const float* __restrict__ g, bf16* __restrict__ out,
-                       float* __restrict__ rstd, int M, int H, float eps) {
+                       float* __restrict__ rstd, int M, int H, float eps, int ny, long long ys) {
   __shared__ float red[16];
   float gr[NC][8];
 #pragma unroll
@@ -197,10 +197,13 @@ __global__ void __launch_bounds__(kNormThreads)
       if (col < H) {
         load8f(x + base + col, v[c]);
         if (y) {
-          float t[8];
-          unpack8(*reinterpret_cast<const uint4*>(y + base + col), t);
+          // TP partials (slots in rank order: the same sum on every TP rank)
+          for (int j = 0; j < ny; ++j) {
+            float t[8];
+            unpack8(*reinterpret_cast<const uint4*>(y + j * ys + base + col), t);
 #pragma unroll
-          for (int k = 0; k < 8; ++k) v[c][k] += t[k];
+            for (int k = 0; k < 8; ++k) v[c][k] += t[k];
+          }
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k) ss += v[c][k] * v[c][k];
@@ -223,10 +226,31 @@ __global__ void __launch_bounds__(kNormThreads)
   }
 }
 
-__global__ void residual_add_kernel(const float* x, const bf16* y, float* xo, long long n) {
+__global__ void residual_add_kernel(const float* x, const bf16* y, float* xo, long long n, int ny,
+                                    long long ys) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    xo[i] = x[i] + bf(y[i]);
+       i += (long long)gridDim.x * blockDim.x) {
+    float v = x[i];
+    for (int j = 0; j < ny; ++j) v += bf(y[j * ys + i]);
+    xo[i] = v;
+  }
+}
+
+// 8 elements per thread (16-byte partial loads, 2 x float4 residual / output)
+__global__ void residual_add8_kernel(const float* __restrict__ x, const bf16* __restrict__ y,
+                                     float* __restrict__ xo, long long n8, int ny, long long ys) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n8;
+       i += (long long)gridDim.x * blockDim.x) {
+    float v[8];
+    load8f(x + 8 * i, v);
+    for (int j = 0; j < ny; ++j) {
+      float t[8];
+      unpack8(*reinterpret_cast<const uint4*>(y + j * ys + 8 * i), t);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] += t[k];
+    }
+    store8f(xo + 8 * i, v);
+  }
 }
 
 // RMSNorm backward, one pass; a persistent CTA per SM walks rows
@@ -248,12 +272,14 @@ __global__ void __launch_bounds__(kNormThreads, NC <= 2 ? 2 : 1)
     rmsnorm_bwd_kernel(const bf16* __restrict__ dyb, const float* __restrict__ dyf,
                        const float* __restrict__ x, const float* __restrict__ rstd,
                        const float* __restrict__ g, const float* dres, float* dx,
-                       bf16* __restrict__ dxb, float* __restrict__ dg_part, int M, int H, int nst) {
+                       bf16* __restrict__ dxb, float* __restrict__ dg_part, int M, int H, int nst,
+                       int ny, long long ys) {
   extern __shared__ uint8_t nsm_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(nsm_raw) + 127) & ~uintptr_t(127));
   __shared__ float red[16];
   __shared__ __align__(8) uint64_t full[kNormStages];
-  const uint32_t xb = uint32_t(H) * 4, yb = uint32_t(H) * (kDyBf16 ? 2 : 4);
+  // dy: ny bf16 TP partial slots (summed in slot order), or one fp32 row
+  const uint32_t xb = uint32_t(H) * 4, yb = uint32_t(H) * (kDyBf16 ? 2 * ny : 4);
   const uint32_t rb = dres ? uint32_t(H) * 4 : 0;
   const uint32_t stage_bytes = xb + yb + rb;
   const int G = gridDim.x;
@@ -269,9 +295,10 @@ __global__ void __launch_bounds__(kNormThreads, NC <= 2 ? 2 : 1)
     uint8_t* st = sm + size_t(s) * stage_bytes;
     mbar_arrive_expect_tx(&full[s], stage_bytes);
     bulk_load_1d(st, x + row * H, xb, &full[s]);
-    if (kDyBf16)
-      bulk_load_1d(st + xb, dyb + row * H, yb, &full[s]);
-    else
+    if (kDyBf16) {
+      for (int j = 0; j < ny; ++j)
+        bulk_load_1d(st + xb + size_t(j) * H * 2, dyb + j * ys + row * H, uint32_t(H) * 2, &full[s]);
+    } else
       bulk_load_1d(st + xb, dyf + row * H, yb, &full[s]);
     if (dres) bulk_load_1d(st + xb + yb, dres + row * H, rb, &full[s]);
   };
@@ -314,11 +341,14 @@ __global__ void __launch_bounds__(kNormThreads, NC <= 2 ? 2 : 1)
           const float4 xx = lds_f4(sx + col);
           float d4[4];
           if (kDyBf16) {
-            const uint2 w = lds_u2(st + xb + size_t(col) * 2);
-            const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&w.x);
-            const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&w.y);
-            d4[0] = __low2float(a); d4[1] = __high2float(a);
-            d4[2] = __low2float(b); d4[3] = __high2float(b);
+            d4[0] = d4[1] = d4[2] = d4[3] = 0.f;
+            for (int j = 0; j < ny; ++j) {
+              const uint2 w = lds_u2(st + xb + (size_t(j) * H + size_t(col)) * 2);
+              const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&w.x);
+              const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&w.y);
+              d4[0] += __low2float(a); d4[1] += __high2float(a);
+              d4[2] += __low2float(b); d4[3] += __high2float(b);
+            }
           } else {
             const float4 v = lds_f4(st + xb + size_t(col) * 4);
             d4[0] = v.x; d4[1] = v.y; d4[2] = v.z; d4[3] = v.w;
@@ -739,6 +769,22 @@ __global__ void step_tick_kernel(StepParams* sp, float b1, float b2) {
   }
 }
 
+// epoch = (step + 1) << 24 | op: strictly increasing over the run, never 0
+__global__ void tp_sync_kernel(TpPeers p, const StepParams* sp, unsigned op) {
+  const int k = threadIdx.x;
+  if (k >= p.tp || k == p.me) return;
+  const unsigned long long e = ((unsigned long long)(sp->cur_step + 1) << 24) | op;
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.remote[k]), "l"(e) : "memory");
+  unsigned long long v = 0;
+  do {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p.local + k) : "memory");
+  } while (v < e);
+}
+void k_tp_sync(const TpPeers& p, const StepParams* sp, unsigned op, cudaStream_t s) {
+  tp_sync_kernel<<<1, 32, 0, s>>>(p, sp, op);
+}
+
 void k_step_tick(StepParams* sp, float b1, float b2, cudaStream_t s) {
   step_tick_kernel<<<1, 32, 0, s>>>(sp, b1, b2);
 }
@@ -762,29 +808,38 @@ void k_embed_bwd(const int32_t* tok, const float* dx, float* dE, int M, int S, i
 }
 // H <= 4 * 2048 (checked by the executor's model validation)
 void k_rmsnorm_fwd(const float* x, const bf16* y, float* xo, const float* g, bf16* out,
-                   float* rstd, int M, int H, float eps, cudaStream_t s) {
+                   float* rstd, int M, int H, float eps, cudaStream_t s, int ny, long long ys) {
   if (M <= 0) return;
   const int grid = std::min(M, 148 * 8);
   const int nc = (H + kNormChunk - 1) / kNormChunk;
 #define HX_NORM_FWD(NC) \
-  rmsnorm_fwd_kernel<NC><<<grid, kNormThreads, 0, s>>>(x, y, xo, g, out, rstd, M, H, eps)
+  rmsnorm_fwd_kernel<NC><<<grid, kNormThreads, 0, s>>>(x, y, xo, g, out, rstd, M, H, eps, ny, ys)
   if (nc <= 1) HX_NORM_FWD(1);
   else if (nc == 2) HX_NORM_FWD(2);
   else if (nc == 3) HX_NORM_FWD(3);
   else HX_NORM_FWD(4);
 #undef HX_NORM_FWD
 }
-void k_residual_add(const float* x, const bf16* y, float* xo, long long n, cudaStream_t s) {
-  if (n > 0) residual_add_kernel<<<ew_grid(n, 4), 256, 0, s>>>(x, y, xo, n);
+void k_residual_add(const float* x, const bf16* y, float* xo, long long n, cudaStream_t s, int ny,
+                    long long ys) {
+  if (n <= 0) return;
+  const bool vec = n % 8 == 0 && ys % 8 == 0 && (reinterpret_cast<uintptr_t>(x) % 16) == 0 &&
+                   (reinterpret_cast<uintptr_t>(y) % 16) == 0 &&
+                   (reinterpret_cast<uintptr_t>(xo) % 16) == 0;
+  if (vec)
+    residual_add8_kernel<<<ew_grid(n / 8, 1), 256, 0, s>>>(x, y, xo, n / 8, ny, ys);
+  else
+    residual_add_kernel<<<ew_grid(n, 4), 256, 0, s>>>(x, y, xo, n, ny, ys);
 }
 void k_rmsnorm_bwd(const bf16* dyb, const float* dyf, const float* x, const float* rstd,
                    const float* g, const float* dres, float* dx, bf16* dxb, float* dg, int M,
-                   int H, float* dg_part, cudaStream_t s) {
+                   int H, float* dg_part, cudaStream_t s, int ny, long long ys) {
   if (M <= 0) return;
+  if (!dyb) ny = 1;
   // one persistent CTA per SM; each CTA's rows end in one partial dg row
   const int nc = (H + kNormChunk - 1) / kNormChunk;
   const int grid = std::min(M, kRmsBwdCtas);
-  const size_t stage = size_t(H) * (4 + (dyb ? 2 : 4) + (dres ? 4 : 0));
+  const size_t stage = size_t(H) * (4 + (dyb ? 2 * ny : 4) + (dres ? 4 : 0));
   const size_t budget = 200u << 10;
   const int nst = int(std::max<size_t>(1, std::min<size_t>(kNormStages, budget / stage)));
   const size_t smem = stage * nst + 128;
@@ -797,7 +852,7 @@ void k_rmsnorm_bwd(const bf16* dyb, const float* dyf, const float* x, const floa
       attr = true;                                                                          \
     }                                                                                       \
     rmsnorm_bwd_kernel<NC, B><<<grid, kNormThreads, smem, s>>>(dyb, dyf, x, rstd, g, dres, dx, \
-                                                                dxb, dg_part, M, H, nst);   \
+                                                                dxb, dg_part, M, H, nst, ny, ys); \
   } while (0)
 #define HX_NORM_BWD_NC(B)       \
   if (nc <= 1) HX_NORM_BWD(1, B); \

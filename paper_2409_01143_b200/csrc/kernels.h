@@ -68,11 +68,15 @@ void k_embed_fwd(const int32_t* tok, const float* E, float* x, int M, int S, int
 void k_embed_bwd(const int32_t* tok, const float* dx, float* dE, int M, int S, int H,
                  uint32_t* keys, cudaStream_t s);
 
-// xo = x (+ y);  out = bf16(xo * rstd * g);  rstd[m] saved.  xo may alias x only if y==null.
+// xo = x (+ y[0] + ... + y[ny-1]);  out = bf16(xo * rstd * g);  rstd[m] saved.
+// y slots are ys elements apart (TP partial sums, added in slot order).  xo may
+// alias x only if y==null.
 void k_rmsnorm_fwd(const float* x, const bf16* y, float* xo, const float* g, bf16* out,
-                   float* rstd, int M, int H, float eps, cudaStream_t s);
-// xo = x + y (no norm)
-void k_residual_add(const float* x, const bf16* y, float* xo, long long n, cudaStream_t s);
+                   float* rstd, int M, int H, float eps, cudaStream_t s, int ny = 1,
+                   long long ys = 0);
+// xo = x + y[0] + ... + y[ny-1] (no norm)
+void k_residual_add(const float* x, const bf16* y, float* xo, long long n, cudaStream_t s,
+                    int ny = 1, long long ys = 0);
 // dx = dres + rmsnorm_bwd(dy);  dx_bf16 optional copy;  dg += sum_m dy*xhat
 // dy is bf16 if dy_bf16 != null else fp32 (dy_f32)
 // Safe in place (dx == dres): each element is read then written by the same
@@ -81,7 +85,21 @@ void k_residual_add(const float* x, const bf16* y, float* xo, long long n, cudaS
 constexpr int kRmsBwdCtas = 148;
 void k_rmsnorm_bwd(const bf16* dy_bf16, const float* dy_f32, const float* x, const float* rstd,
                    const float* g, const float* dres, float* dx, bf16* dx_bf16, float* dg, int M,
-                   int H, float* dg_part, cudaStream_t s);
+                   int H, float* dg_part, cudaStream_t s, int ny = 1, long long ys = 0);
+// (bf16 dy may be ny TP partial slots, ys elements apart, summed in slot order)
+
+// ---- TP exchange over peer memory ---------------------------------------
+// Every TP rank owns a flag array flags[tp] (uint64, in its IPC-shared
+// exchange buffer).  tp_sync(op): publish epoch(step, op) to flags[me] of every
+// peer (release, system scope), then wait until every peer's flag in the local
+// array reached it (acquire).  Kernel boundaries order it after the producing
+// GEMM (whose TMA stores already reached the peers) and before the consumer.
+struct TpPeers {
+  unsigned long long* remote[4];  // remote[k] = &flags_of_rank_k[me] (k != me)
+  unsigned long long* local;      // this rank's flags[tp]
+  int tp, me;
+};
+void k_tp_sync(const TpPeers& p, const StepParams* sp, unsigned op, cudaStream_t s);
 
 // in-place rotary embedding of q and k inside the fused [M, nh*3*d] buffer
 // (rotate-half convention); inverse=1 applies the transpose (backward).
