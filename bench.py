@@ -40,8 +40,16 @@ METRIC = "tokens/s & MFU per asym plan at 1/2/4/8 B200 vs even split + CPU ref"
 PLANS = {
     1: ("llama7b_4l_1gpu", None),
     2: ("llama7b_4l_tp31", "llama7b_4l_tp11_eq,llama7b_4l_2_even"),
-    4: ("llama7b_4l_4_asym", "llama7b_4l_4_even"),
-    8: ("llama7b_8_asym", "llama7b_8_eq_even"),
+    4: ("llama7b_4l_4_cal", "llama7b_4l_4_even"),
+    8: ("llama7b_8_cal", "llama7b_8_eq_even"),
+}
+# further asymmetric arms reported beside the headline one: the nominal-tier
+# planner plans (peak_tflops proportional to the SM share) and, for cfg2, the
+# TP widths chosen from the calibrated speeds
+ALT = {
+    2: "llama7b_4l_tp52,llama7b_4l_2_cal",
+    4: "llama7b_4l_4_asym",
+    8: "llama7b_8_asym",
 }
 B200_SPEC = 2250.0
 
@@ -118,6 +126,7 @@ class Clocks:
         self.f.flush()
         rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
         sm, mx, reasons = [], [], set()
+        per = {}
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in rows:
             r = [x.strip() for x in r]
@@ -127,6 +136,7 @@ class Clocks:
                     continue
                 sm.append(float(r[2]))
                 mx.append(float(r[3]))
+                per.setdefault(r[1], []).append(float(r[2]))
             except (ValueError, IndexError):
                 continue
             for i, n in enumerate(names):
@@ -135,6 +145,7 @@ class Clocks:
         os.unlink(self.f.name)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "sm_mhz_per_gpu": {k: statistics.median(v) for k, v in sorted(per.items())},
                 "samples": len(sm)}
 
 
@@ -362,6 +373,7 @@ def main():
                     help="comma-separated even-split comparison plans ('none' to skip)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-alt", action="store_true", help="skip the extra asymmetric arms")
     ap.add_argument("--exec-config", default="{}", help="JSON executor config overrides")
     a = ap.parse_args()
     EXEC_CFG.update(json.loads(a.exec_config))
@@ -408,10 +420,15 @@ def main():
     r = run_plan(asym, a.steps, a.warmup, rank, world, clocks=(rank == 0))
     s = summarize(r, a.steps, pk)
     ev = None
+    alts = []
+    for a_name in (ALT.get(a.gpus, "").split(",") if not a.plan and not a.no_alt else []):
+        if a_name:
+            ra = run_plan(a_name, a.steps, a.warmup, rank, world, clocks=(rank == 0))
+            alts.append(dict(summarize(ra, a.steps, pk), clocks=ra["clocks"]))
     evs = []
     for e_name in (even.split(",") if even else []):
-        re_ = run_plan(e_name, a.steps, a.warmup, rank, world, clocks=False)
-        evs.append(summarize(re_, a.steps, pk))
+        re_ = run_plan(e_name, a.steps, a.warmup, rank, world, clocks=(rank == 0))
+        evs.append(dict(summarize(re_, a.steps, pk), clocks=re_["clocks"]))
     ev = evs[0] if evs else None
     if rank != 0:
         return
@@ -446,6 +463,7 @@ def main():
                 "aggregate_sm_share": s["aggregate_sm_share"]},
         "even_split": ev,
         "even_split_other": evs[1:],
+        "asym_other": alts,
         "mfu_gap_vs_even": (ev["mfu_ref_convention"] - s["mfu_ref_convention"]) if ev else None,
         "e2e": {"value": s["e2e_tokens_per_s"], "unit": "tokens/s",
                 "h2d_bytes_per_step": int(r["h2d"]), "d2h_bytes_per_step": int(r["d2h"])},
@@ -483,6 +501,11 @@ INDEX_DESC = {
                          "tiers [F,F,1/2,1/2]",
     "llama7b_8_asym": "Llama-7B (32 layers) on 8xB200 tiers [F,F,F,F,1/2,1/2,1/3,1/3]: "
                       "hexplan_schedule plan, asymmetric DP 15/12/12/12/13",
+    "llama7b_4l_4_cal": "Llama-7B-shaped 4-layer block, hexplan_schedule plan on 4xB200 tiers "
+                        "[F,F,1/2,1/2] with calibrated tier speeds: asymmetric DP 14/14/10/10",
+    "llama7b_8_cal": "Llama-7B (32 layers) on 8xB200 tiers [F,F,F,F,1/2,1/2,1/3,1/3] with "
+                     "calibrated tier speeds: hexplan_schedule plan, asymmetric DP 21/21/22 over "
+                     "PP 16/16, 16/16 and TP=2 stages 20/12",
     "llama13b_pp3_asymtp": "Llama-13B 3-stage pipeline 16/14/10, asymmetric TP inside stages",
     "llama30b_8_tiers": "Llama-30B layers under a full hexplan_schedule plan, 8xB200 SM-capped tiers",
 }

@@ -19,16 +19,28 @@ HERE = os.path.join(ROOT, "configs")
 sys.path.insert(0, ROOT)
 
 F, HALF, THIRD = 2250.0, 1125.0, 750.0
+# Closed-loop calibration: effective speeds of the SM-capped
+# tiers measured on B200 (bench.py reference_cost_model.calibrated, r01:
+# llama7b_4l_4_asym -> F 1258 / 1278, H 910 / 909; llama7b_4l_2_asym -> F 1271,
+# T 525).  Power capping makes a capped B200 faster per SM than a full one
+# (SM clocks 1940-1965 vs ~1450 MHz), so the tiers are not 1 : 1/2 : 1/3.
+F_CAL, HALF_CAL, THIRD_CAL = 1270.0, 909.0, 525.0
 
 
-def cluster(devs, machines=None):
+def cluster(devs, machines=None, sm=None):
+    """devs: [(id, peak_tflops)]; sm: {id: sm_fraction} pins the SM cap (the
+    calibrated documents keep the nominal tiers' caps, SURVEY 8(b) extension)"""
     machines = machines or {"box": [d for d, _ in devs]}
     mdoc = {m: {"intra_bandwidth_gbps": 900, "intra_latency_us": 3} for m in machines}
     where = {d: m for m, ds in machines.items() for d in ds}
-    return {"machines": mdoc,
-            "devices": [{"id": d, "machine": where[d], "memory_gib": 178, "peak_tflops": p}
-                        for d, p in devs],
-            "inter": {"bandwidth_gbps": 900, "latency_us": 3}}
+    out = {"machines": mdoc,
+           "devices": [{"id": d, "machine": where[d], "memory_gib": 178, "peak_tflops": p}
+                       for d, p in devs],
+           "inter": {"bandwidth_gbps": 900, "latency_us": 3}}
+    for d in out["devices"]:
+        if sm and d["id"] in sm:
+            d["sm_fraction"] = sm[d["id"]]
+    return out
 
 
 TIERS8 = [("g0", F), ("g1", F), ("g2", F), ("g3", F), ("g4", HALF), ("g5", HALF),
@@ -48,6 +60,15 @@ CLUSTERS = {
     "b200_2_eq": cluster([(f"g{i}", (F + THIRD) / 2) for i in range(2)]),
     "b200_4_eq": cluster([(f"g{i}", (2 * F + 2 * HALF) / 4) for i in range(4)]),
     "b200_8_eq": cluster([(f"g{i}", (4 * F + 2 * HALF + 2 * THIRD) / 8) for i in range(8)]),
+    # calibrated tier speeds, same SM caps as the nominal tier clusters
+    "b200_2_capped_cal": cluster([("g0", F_CAL), ("g1", THIRD_CAL)], sm={"g0": 1.0, "g1": 1 / 3}),
+    "b200_4_tiers_cal": cluster([("g0", F_CAL), ("g1", F_CAL), ("g2", HALF_CAL), ("g3", HALF_CAL)],
+                                sm={"g0": 1.0, "g1": 1.0, "g2": 0.5, "g3": 0.5}),
+    "b200_8_onebox_cal": cluster(
+        [("g0", F_CAL), ("g1", F_CAL), ("g2", F_CAL), ("g3", F_CAL), ("g4", HALF_CAL),
+         ("g5", HALF_CAL), ("g6", THIRD_CAL), ("g7", THIRD_CAL)],
+        sm={"g0": 1.0, "g1": 1.0, "g2": 1.0, "g3": 1.0, "g4": 0.5, "g5": 0.5, "g6": 1 / 3,
+            "g7": 1 / 3}),
 }
 
 MODELS = {
@@ -106,6 +127,18 @@ HAND = {
                         plan([pipe(8, 1, [stage(["g0", "g1"], 0, 4, [3, 1])])], 4)),
     "llama7b_4l_tp11_even": ("b200_2_even", "llama7b_4l",
                              plan([pipe(8, 1, [stage(["g0", "g1"], 0, 4)])], 4)),
+    # the equivalent even-split of cfg2: TP=2 with equal widths on two
+    # homogeneous devices of the same aggregate compute
+    "llama7b_4l_tp11_eq": ("b200_2_eq", "llama7b_4l",
+                           plan([pipe(8, 1, [stage(["g0", "g1"], 0, 4)])], 4)),
+    # 4-GPU analogue of the calibrated 8-GPU plan's structure at full 7B size:
+    # PP 16/16 on the F pair, TP=2 over the H pair, DP across mismatched TP
+    "llama7b_4_mix": ("b200_4_tiers_cal", "llama7b", plan([
+        pipe(20, 1, [stage(["g0"], 0, 16), stage(["g1"], 16, 16)]),
+        pipe(12, 1, [stage(["g2", "g3"], 0, 32)])], 32)),
+    # cfg2 with widths from the calibrated speeds (1270 : 525 ~ 5 : 2)
+    "llama7b_4l_tp52": ("b200_2_capped", "llama7b_4l",
+                        plan([pipe(8, 1, [stage(["g0", "g1"], 0, 4, [5, 2])])], 4)),
     # cfg4: Llama-13B, 3 stages 16/14/10, asymmetric TP inside stages
     "llama13b_pp3_asymtp": ("b200_8_onebox", "llama13b", plan([pipe(16, 1, [
         stage(["g0", "g1", "g4"], 0, 16, [2, 2, 1]),
@@ -132,6 +165,16 @@ PLANNED = {
     "llama7b_4l_2_asym": ("b200_2_capped", "llama7b_4l", "schedule",
                           {"global_batch": 8, "iterations": 20, "seed": 0, "threads": 8,
                            "state_multiplier": 2.5}),
+    # the reference scheduler on the calibrated tier speeds
+    "llama7b_4l_2_cal": ("b200_2_capped_cal", "llama7b_4l", "schedule",
+                         {"global_batch": 8, "iterations": 20, "seed": 0, "threads": 8,
+                          "state_multiplier": 2.5}),
+    "llama7b_4l_4_cal": ("b200_4_tiers_cal", "llama7b_4l", "schedule",
+                         {"global_batch": 48, "iterations": 30, "seed": 0, "threads": 8,
+                          "state_multiplier": 2.5}),
+    "llama7b_8_cal": ("b200_8_onebox_cal", "llama7b", "schedule",
+                      {"global_batch": 64, "iterations": 50, "seed": 0, "threads": 8,
+                       "state_multiplier": 2.5}),
     # even-split plans (hexplan_symmetric_baseline) at equal aggregate compute
     "llama7b_4l_2_even": ("b200_2_eq", "llama7b_4l", "symmetric",
                           {"global_batch": 8, "iterations": 20, "seed": 0, "threads": 8,
