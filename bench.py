@@ -146,6 +146,7 @@ class Clocks:
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
                 "sm_mhz_per_gpu": {k: statistics.median(v) for k, v in sorted(per.items())},
+                "gpu_of_rank": self.ids.split(","),
                 "samples": len(sm)}
 
 
@@ -285,7 +286,26 @@ def summarize(r: dict, steps: int, pk: dict) -> dict:
             "ms_per_step": r["dev_ms"] / steps, "e2e_ms_per_step": r["e2e_ms"] / steps,
             "mfu_ref_convention": ref_f / step_s / agg if agg else None,
             "mfu_exact": exact_f / step_s / agg if agg else None,
-            "aggregate_sm_share": r["sm_share"], "loss": r["loss"]}
+            "aggregate_sm_share": r["sm_share"], "loss": r["loss"],
+            "sm_ghz": sm_ghz(r), "tokens_per_s_per_sm_ghz": tps / sm_ghz(r) if sm_ghz(r) else None}
+
+
+def sm_ghz(r: dict):
+    """Delivered compute capacity of the job: sum over ranks of applied SMs x
+    median SM clock in the timed region (GHz).  Under the B200 power cap a
+    full-SM rank clocks ~1.45-1.55 GHz while an SM-capped one holds ~1.95 GHz,
+    so SM shares alone overstate a full B200 against a capped one; tokens/s per
+    SM-GHz compares plans on what the hardware actually delivered."""
+    ck = r.get("clocks") or {}
+    clk = ck.get("sm_mhz_per_gpu") or {}
+    ids = ck.get("gpu_of_rank") or []
+    tot = 0.0
+    for rank, (_, _, _, share) in enumerate(r.get("lin_per_rank") or []):
+        mhz = clk.get(ids[rank]) if rank < len(ids) else None
+        if mhz is None:
+            return None
+        tot += share * 148 * mhz / 1e3
+    return tot or None
 
 
 def reference_cost(name: str, seconds: float | None, speeds=None):
