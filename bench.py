@@ -484,6 +484,7 @@ def main():
         "even_split": ev,
         "even_split_other": evs[1:],
         "asym_other": alts,
+        "sm_ghz": s["sm_ghz"], "tokens_per_s_per_sm_ghz": s["tokens_per_s_per_sm_ghz"],
         "mfu_gap_vs_even": (ev["mfu_ref_convention"] - s["mfu_ref_convention"]) if ev else None,
         "e2e": {"value": s["e2e_tokens_per_s"], "unit": "tokens/s",
                 "h2d_bytes_per_step": int(r["h2d"]), "d2h_bytes_per_step": int(r["d2h"])},

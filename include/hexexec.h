@@ -143,6 +143,9 @@ hexexec_status hexexec_k_gemm_split(int split, float* ws, size_t ws_bytes, int* 
  * TMA-stored to peers[k] (device pointers with C's layout, e.g. another GPU's
  * buffer reachable over NVLink); n = 0 clears.  At most 3. */
 hexexec_status hexexec_k_gemm_peers(void* const* peers, int n);
+/* tile raster of every later GEMM (process-wide): bands of group_m M-tiles
+ * walked M-fastest (default 8); 0 = N-fastest (tuning / microbenchmarks) */
+hexexec_status hexexec_k_gemm_raster(int group_m);
 /* fused causal attention over the head-interleaved QKV buffer [mb*S, nh*3*d]:
  * out [mb*S, nh*d] bf16, lse [mb*nh, S] (log2 domain); backward writes
  * dq/dk/dv into dqkv [mb*S, nh*3*d] (delta / dq_acc: fp32 scratch of

@@ -74,5 +74,7 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream);
 void gemm_set_sm_limit(int sms);
 // 0 = auto (CTA pairs when M > 128), 1 / 2 = force single-SM / paired tiles
 void gemm_force_cta_group(int cg);
+// grouped tile raster: bands of g M-tiles (default 8); 0 = n fastest
+void gemm_set_group_m(int g);
 
 }  // namespace hexexec

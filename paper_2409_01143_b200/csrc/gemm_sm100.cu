@@ -48,6 +48,7 @@ struct EpiParams {
   float* ws;         // [split tiles][TM][BN] fp32
   int* ws_cnt;       // per (split tile, 32-row slab)
   int npeer;         // extra copies of every stored C tile (TP peers' buffers)
+  int group_m;       // grouped tile raster (M-tiles per band), 0 = n fastest
 };
 
 // TMA maps of the peer copies of C (IPC-mapped buffers of the other TP ranks,
@@ -127,14 +128,28 @@ HX_DEVICE void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// tile t -> (m0, n-tile index, batch coords); n fastest so CTAs of one wave
-// share the A row-panel in L2
+// tile t -> (m0, n-tile index, batch coords).  group_m > 0: grouped raster,
+// bands of group_m M-tiles walked M-fastest, so one wave of P pairs covers a
+// ~group_m x P/group_m block and both operand panels are re-read from L2
+// (n-fastest over a wide N would stream every B panel from HBM once per
+// M-tile: 8x the B bytes at M = 2048).  group_m = 0: n fastest.
 template <int TM>
 HX_DEVICE void decode_tile(const EpiParams& p, int t, int& m0, int& nt, int& z1, int& z2) {
-  nt = t % p.n_tiles;
-  int r = t / p.n_tiles;
-  m0 = (r % p.m_tiles) * TM;
-  int z = r / p.m_tiles;
+  const int per_batch = p.m_tiles * p.n_tiles;
+  const int z = t / per_batch;
+  const int r = t - z * per_batch;
+  if (p.group_m > 0) {
+    const int per_group = p.group_m * p.n_tiles;
+    const int g = r / per_group;
+    const int first = g * p.group_m;
+    const int gm = min(p.group_m, p.m_tiles - first);
+    const int q = r - g * per_group;
+    m0 = (first + q % gm) * TM;
+    nt = q / gm;
+  } else {
+    nt = r % p.n_tiles;
+    m0 = (r / p.n_tiles) * TM;
+  }
   z1 = z % p.nb1;
   z2 = z / p.nb1;
 }
@@ -540,6 +555,7 @@ std::once_flag g_encode_once;
 int g_sm_limit = 0;
 int g_num_sms = 0;
 int g_force_cg = 0;  // 0 = auto, 1 / 2 = force (tests)
+int g_group_m = 8;   // grouped raster band height in M-tiles (0 = n fastest)
 
 cudaError_t load_encode() {
   std::call_once(g_encode_once, [] {
@@ -667,6 +683,7 @@ int choose_split(int T, int P, int kblocks, bool direct) {
 
 void gemm_set_sm_limit(int sms) { g_sm_limit = sms; }
 void gemm_force_cta_group(int cg) { g_force_cg = cg; }
+void gemm_set_group_m(int g) { g_group_m = std::max(0, g); }
 
 cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream) {
   cudaError_t e = load_encode();
@@ -709,6 +726,7 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream) {
   p.m_tiles = (d.M + TM - 1) / TM;
   p.n_tiles = (d.N + BN - 1) / BN;
   p.num_tiles = p.m_tiles * p.n_tiles * d.nb1 * d.nb2;
+  p.group_m = d.causal == kCausalNone ? std::min(p.m_tiles, g_group_m) : 0;
   if (d.beta && !d.c_fp32) return cudaErrorInvalidValue;
   CUtensorMap mc, mr;
   if (!make_map_c(&mc, d.C, d.c_fp32, d.N, d.M, d.ldc, d.cbs1, d.cbs2, d.nb1, d.nb2))
