@@ -79,6 +79,7 @@ ExecConfig parse_exec_config(const std::string& text) {
       else if (k == "tp_reduce") c.tp_reduce = v.get<std::string>();
       else if (k == "tp_direction") c.tp_direction = v.get<std::string>();
       else if (k == "graph_gemm_events") c.graph_gemm_events = v.get<bool>();
+      else if (k == "fuse_swiglu") c.fuse_swiglu = v.get<bool>();
       else throw ParseError("exec config: unknown key '" + k + "'");
     } catch (const nlohmann::json::exception& e) {
       throw ParseError("exec config: bad value for '" + k + "'");
@@ -941,10 +942,16 @@ class Executor {
       k_rmsnorm_fwd(x_in, ypart, a.x_mid, w.mlp_norm.p32, a.hn, a.rstd2, int(M), int(H), eps, stream);
       kcheck("rmsnorm_fwd");
     }
-    // MLP block
-    gemm(g2(M, 2 * F, H, a.hn, 0, H, w.wgu.p16, 0, H, a.gu, 2 * F, 0));
-    k_swiglu_fwd(a.gu, a.act, int(M), int(F), stream);
-    kcheck("swiglu_fwd");
+    // MLP block: gate-up GEMM with the SwiGLU epilogue (act written from the tile)
+    {
+      GemmDesc g = g2(M, 2 * F, H, a.hn, 0, H, w.wgu.p16, 0, H, a.gu, 2 * F, 0);
+      if (cfg.fuse_swiglu) g.act = a.act;
+      gemm(g);
+      if (!cfg.fuse_swiglu) {
+        k_swiglu_fwd(a.gu, a.act, int(M), int(F), stream);
+        kcheck("swiglu_fwd");
+      }
+    }
     if (recompute) return;
     if (role.tp == 1) {
       GemmDesc g = g2(M, H, F, a.act, 0, F, w.wdown.p16, 1, H, x_out, H, 1);

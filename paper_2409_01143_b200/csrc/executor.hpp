@@ -19,6 +19,7 @@ struct ExecConfig {
   bool validate_only = false;
   bool profile_gemm = false;          // per-GEMM CUDA events (roofline evidence); eager
   bool graph_gemm_events = false;     // per-GEMM CUDA events inside the step graph
+  bool fuse_swiglu = true;            // SwiGLU in the gate-up GEMM epilogue
   bool cuda_graph = true;             // replay the captured step graph (after step 0)
   std::string attention = "fused";    // "fused" (flash, tcgen05) | "unfused" (GEMM+softmax)
   bool dp_overlap = true;             // DP sync + AdamW per layer on a second stream

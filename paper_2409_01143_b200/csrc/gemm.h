@@ -60,6 +60,12 @@ struct GemmDesc {
   // so the row-parallel partials cross NVLink while the GEMM still runs)
   void* peer_C[kMaxGemmPeers] = {nullptr, nullptr, nullptr};
   int npeer = 0;
+  // SwiGLU epilogue (gate-up projection): C holds [g | u] in 128-column chunk
+  // pairs (64 gate, 64 up); act[m, f] = silu(g) * u (bf16, [M, N/2], row
+  // stride ld_act or N/2) is written from the same tile.  bf16 C, no beta /
+  // split / peers / batch.
+  void* act = nullptr;
+  long long ld_act = 0;
 };
 
 // workspace a GemmDesc needs for any split (bytes, counters)

@@ -49,6 +49,7 @@ struct EpiParams {
   int* ws_cnt;       // per (split tile, 32-row slab)
   int npeer;         // extra copies of every stored C tile (TP peers' buffers)
   int group_m;       // grouped tile raster (M-tiles per band), 0 = n fastest
+  int act_mode;      // 1: SwiGLU epilogue, act = silu(g) * u to pm.m[0]
 };
 
 // TMA maps of the peer copies of C (IPC-mapped buffers of the other TP ranks,
@@ -382,7 +383,51 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row0 = m0 + BM * int(crank) + ew * 32;  // this warp's 32-row slab
-      if (row0 < p.M) {
+      if (row0 < p.M && p.act_mode) {
+        // SwiGLU epilogue: C columns come in 128-wide (64 gate | 64 up) chunk
+        // pairs; per 32-column half: store g and u (bf16) to C and
+        // act = silu(g) * u, from the bf16-rounded g and u exactly as
+        // swiglu_fwd_kernel computes it, to the act map (pm.m[0], [M, N/2]).
+        // Each 4 KB staging buffer holds two bf16 chunks: 3 stores per
+        // half, double-buffered over the 3 buffers.
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 128) {
+          if (n0 + c >= p.N) break;
+#pragma unroll 1
+          for (int h = 0; h < 64; h += 32) {
+            uint32_t rg[32], ru[32];
+            const uint32_t tcol = tbase + (uint32_t(ew * 32) << 16) + uint32_t(acc * BN + c + h);
+            tmem_ld_32x32b_x32(tcol, rg);
+            tmem_ld_32x32b_x32(tcol + 64, ru);
+            tmem_ld_wait();
+            float g[32], uu[32], a[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              g[i] = __bfloat162float(__float2bfloat16(__uint_as_float(rg[i]) * p.alpha));
+              uu[i] = __bfloat162float(__float2bfloat16(__uint_as_float(ru[i]) * p.alpha));
+              a[i] = g[i] * (1.f / (1.f + __expf(-g[i]))) * uu[i];
+            }
+            // the slot set written now was read by the stores two halves ago
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+            uint8_t* b0 = ebuf + sb * (C::EPI_CHUNK / 2);  // slots sb, sb+2, sb+4 (2 KB each)
+            uint8_t* b1 = b0 + C::EPI_CHUNK;
+            uint8_t* b2 = b1 + C::EPI_CHUNK;
+            stage_chunk(b0, g, false, lane);
+            stage_chunk(b1, uu, false, lane);
+            stage_chunk(b2, a, false, lane);
+            fence_async_shared();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_4d(&tmC, b0, n0 + c + h, row0, z1, z2);
+              tma_store_4d(&tmC, b1, n0 + c + 64 + h, row0, z1, z2);
+              tma_store_4d(&pm.m[0], b2, (n0 + c) / 2 + h, row0, z1, z2);
+              bulk_commit();
+            }
+            sb ^= 1;
+          }
+        }
+      } else if (row0 < p.M) {
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           const int col = n0 + c;
@@ -740,12 +785,17 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream) {
   static_assert(sizeof(PeerMaps) == kMaxGemmPeers * sizeof(CUtensorMap), "PeerMaps layout");
   PeerMaps pm;
   p.npeer = d.npeer;
+  p.act_mode = d.act ? 1 : 0;
+  if (d.act && (d.npeer || d.beta || d.c_fp32 || d.R || d.N % 128 || d.nb1 * d.nb2 != 1))
+    return cudaErrorInvalidValue;
   if (d.npeer < 0 || d.npeer > kMaxGemmPeers) return cudaErrorInvalidValue;
   if (d.npeer && (d.beta || d.c_fp32)) return cudaErrorInvalidValue;
   for (int k = 0; k < d.npeer; ++k)
     if (!make_map_c(&pm.m[k], d.peer_C[k], 0, d.N, d.M, d.ldc, d.cbs1, d.cbs2, d.nb1, d.nb2))
       return cudaErrorInvalidValue;
   for (int k = d.npeer; k < kMaxGemmPeers; ++k) pm.m[k] = mc;
+  if (d.act && !make_map_c(&pm.m[0], d.act, 0, d.N / 2, d.M, d.ld_act ? d.ld_act : d.N / 2, 0, 0, 1, 1))
+    return cudaErrorInvalidValue;
   const int sms = g_sm_limit > 0 ? std::min(g_sm_limit, g_num_sms) : g_num_sms;
   const int P = std::max(1, sms / CG);
   // tail split (dense GEMMs only)
@@ -756,7 +806,7 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream) {
   p.ws = d.ws;
   p.ws_cnt = d.ws_cnt;
   CUtensorMap mw = mc;
-  if (d.causal == kCausalNone && d.split != 0 && d.npeer == 0 && p.num_tiles > 0) {
+  if (d.causal == kCausalNone && d.split != 0 && d.npeer == 0 && !d.act && p.num_tiles > 0) {
     const int kblocks = (d.K + BK - 1) / BK;
     const bool direct = d.beta && !d.R;
     int s = d.split > 1 ? std::min(d.split, std::max(1, kblocks))

@@ -210,3 +210,17 @@ def test_tp_peer_exchange_matches_nccl(tmp_path, name):
         for c in copies[1:]:
             if c.shape == copies[0].shape:
                 assert np.array_equal(c, copies[0]), key
+
+
+@pytest.mark.parametrize("name", ["tiny_1", "tiny_tp31"])
+def test_swiglu_epilogue_matches_kernel(tmp_path, name):
+    """SwiGLU computed in the gate-up GEMM epilogue (act from the bf16-rounded
+    g, u of the tile) == the standalone swiglu_fwd kernel on the stored gu."""
+    fused = run_plan(name, tmp_path / "fused", steps=2, xcfg={"fuse_swiglu": True})
+    plain = run_plan(name, tmp_path / "plain", steps=2, xcfg={"fuse_swiglu": False})
+    check_against_oracle(name, fused)
+    for a, b in zip(fused, plain):
+        assert np.allclose(a["losses"], b["losses"], rtol=1e-6, atol=0), (a["losses"], b["losses"])
+        for key in a:
+            if key.endswith("|w"):
+                assert np.allclose(a[key], b[key], rtol=1e-5, atol=1e-6), key
