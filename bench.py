@@ -261,6 +261,9 @@ def run_plan(name: str, steps: int, warmup: int, rank: int, world: int, clocks: 
     share = float(st["sm_applied"]) / max(float(st["sm_total"]), 1.0) if role["active"] else 0.0
     tl_all = gather_all({k: round(v["ms"] / 2, 3) for k, v in st.get("timeline_ms", {}).items()},
                         rank, world, f"tl-{name}")
+    tlg_all = gather_all({k: round(v["ms"], 4) for k, v in
+                          st_timed.get("timeline_graph_one_mb", {}).items()}, rank, world,
+                         f"tlg-{name}")
     per_rank = gather_all([float(lin.get("flops", 0.0)), float(lin.get("ms", 0.0)),
                            float(lin.get("launches", 0)), share], rank, world, f"lin-{name}")
     ex.close()
@@ -268,7 +271,7 @@ def run_plan(name: str, steps: int, warmup: int, rank: int, world: int, clocks: 
     return dict(name=name, idx=idx, cluster=json.loads(c), model=json.loads(m),
                 plan=json.loads(p), dev_ms=dev_ms, e2e_ms=e2e_ms, loss=loss, clocks=clk,
                 stats=st, gemm_graph=gg, h2d=sums[0], d2h=sums[1], launches=sums[2], lin_flops=sums[3],
-                lin_ms=sums[4], lin_launches=sums[5], sm_share=sums[6], lin_per_rank=per_rank, tl_all=tl_all,
+                lin_ms=sums[4], lin_launches=sums[5], sm_share=sums[6], lin_per_rank=per_rank, tl_all=tl_all, tlg_all=tlg_all,
                 speeds=[x for x in speeds if x])
 
 
@@ -505,6 +508,7 @@ def main():
         "phase_ms_rank0": r["stats"].get("ms"),
         "timeline_ms_rank0_profiled": r["stats"].get("timeline_ms"),
         "timeline_ms_per_step_per_rank_profiled": r["tl_all"] if a.gpus > 1 else None,
+        "timeline_ms_one_microbatch_per_rank_graph": r["tlg_all"],
         "sm_cap_rank0": {k: r["stats"].get(k) for k in ("sm_cap_mode", "sm_applied", "sm_total")},
         "clocks": r["clocks"],
         "cpu_baseline": cpu,

@@ -282,6 +282,8 @@ class Executor {
     }
     graph_recs_.clear();
     graph_shapes_.clear();
+    for (auto& m : gmarks_) cudaEventDestroy(m.ev);
+    gmarks_.clear();
     if (gexec_) cudaGraphExecDestroy(gexec_);
     gexec_ = nullptr;
     for (auto& g : groups_)
@@ -643,7 +645,32 @@ class Executor {
   std::vector<cudaEvent_t> mark_pool_;
   std::vector<Mark> marks_;
   std::map<std::string, std::pair<double, int64_t>> timeline_;
+  // graph timeline (graph_gemm_events): the same marks captured as event
+  // nodes for the sampled micro-batch's forward and backward; an op's time is
+  // the distance to the previous mark of the same contiguous run
+  struct GMark {
+    cudaEvent_t ev;
+    const char* kind;
+    int run;
+  };
+  std::vector<GMark> gmarks_;
+  int gmark_run_ = 0;
+  int64_t gmark_last_mb_ = -1;
+  bool gmark_last_bwd_ = false;
+  bool in_bwd_ = false;
   void mark(const char* kind) {
+    if (capturing_ && cfg.graph_gemm_events && cur_mb_ == role.n_mb / 2) {
+      if (cur_mb_ != gmark_last_mb_ || in_bwd_ != gmark_last_bwd_ || gmarks_.empty()) {
+        ++gmark_run_;  // a new run starts with a reference mark
+        gmark_last_mb_ = cur_mb_;
+        gmark_last_bwd_ = in_bwd_;
+      }
+      cudaEvent_t e;
+      HX_CUDA(cudaEventCreate(&e));
+      HX_CUDA(cudaEventRecordWithFlags(e, stream, cudaEventRecordExternal));
+      gmarks_.push_back({e, kind, gmark_run_});
+      return;
+    }
     if (!cfg.profile_gemm) return;
     if (marks_.size() == mark_pool_.size()) {
       cudaEvent_t e;
@@ -1055,6 +1082,8 @@ class Executor {
 
   void forward(int64_t mbi, Slot& sl) {
     cur_mb_ = mbi;
+    in_bwd_ = false;
+    mark("fwd_begin");
     if (role.first_stage) {
       k_embed_fwd(tok_of(mbi), embed.p32, sl.x[0], int(M), int(S), int(H), stream);
       kcheck("embed_fwd");
@@ -1207,6 +1236,8 @@ class Executor {
   // (received), or null on the last stage (starts from dlogits)
   void backward(int64_t mbi, Slot& sl, float* dx_top) {
     cur_mb_ = mbi;
+    in_bwd_ = true;
+    mark("bwd_begin");
     float* cur = dx[0];
     float* nxt = dx[1];
     bf16* curb = dxb;
@@ -1670,6 +1701,21 @@ class Executor {
       ojson tl;
       for (const auto& [k, v] : timeline_) tl[k] = {{"ms", v.first}, {"ops", v.second}};
       j["timeline_ms"] = tl;
+    }
+    if (!gmarks_.empty()) {
+      std::map<std::string, std::pair<double, int64_t>> t;
+      for (size_t i = 1; i < gmarks_.size(); ++i) {
+        if (gmarks_[i].run != gmarks_[i - 1].run) continue;
+        float ms = 0;
+        if (cudaEventElapsedTime(&ms, gmarks_[i - 1].ev, gmarks_[i].ev) != cudaSuccess) continue;
+        auto& v = t[gmarks_[i].kind];
+        v.first += ms;
+        v.second += 1;
+      }
+      (void)cudaGetLastError();
+      ojson tl;
+      for (const auto& [k, v] : t) tl[k] = {{"ms", v.first}, {"ops", v.second}};
+      j["timeline_graph_one_mb"] = tl;
     }
     if (!graph_recs_.empty()) {
       const char* names[3] = {"tp_linear", "attention", "lm_head"};
