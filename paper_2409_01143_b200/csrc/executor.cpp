@@ -80,6 +80,7 @@ ExecConfig parse_exec_config(const std::string& text) {
       else if (k == "tp_direction") c.tp_direction = v.get<std::string>();
       else if (k == "graph_gemm_events") c.graph_gemm_events = v.get<bool>();
       else if (k == "fuse_swiglu") c.fuse_swiglu = v.get<bool>();
+      else if (k == "wgrad_group") c.wgrad_group = v.get<int>();
       else throw ParseError("exec config: unknown key '" + k + "'");
     } catch (const nlohmann::json::exception& e) {
       throw ParseError("exec config: bad value for '" + k + "'");
@@ -223,6 +224,25 @@ class Executor {
   unsigned xop_ = 0;
   bool tp_peer_ = false;
   int tp_crit_ = -1;  // TP index of the critical (slowest) rank, or -1
+  // Weight-gradient grouping (wgrad_group): the operands of the four layer
+  // weight-gradient GEMMs (and the LM head's) of G consecutive micro-batches
+  // are kept token-concatenated, and one GEMM with K = G*M per weight runs at
+  // the group's last backward -- one fp32 store instead of G fp32 reduce-adds
+  // of the gradient.  nbuf ring buffers of G micro-batch rows each.
+  struct WStash {
+    bf16 *act, *hn, *attn, *xn, *dxob, *dgu, *dxmb, *dqkv;
+  };
+  int64_t wg_ = 1, wg_nbuf_ = 1;
+  std::vector<WStash> wst_;      // [nbuf][nl]
+  std::vector<bf16*> wst_xf_, wst_dlog_;  // [nbuf]
+  int64_t wg_bytes_per_mb() const {
+    int64_t w = nl * (3 * F + 4 * H + kr + qkvw);
+    if (role.last_stage) w += H + Vr;
+    return 2 * M * w;
+  }
+  WStash& ws(int64_t l, int64_t mbi) { return wst_[size_t(((mbi / wg_) % wg_nbuf_) * nl + l)]; }
+  bf16* wrow(bf16* base, int64_t mbi, int64_t width) const { return base + (mbi % wg_) * M * width; }
+  bool wg_end(int64_t mbi) const { return mbi % wg_ == wg_ - 1 || mbi == role.n_mb - 1; }
   float* recv_buf = nullptr;  // fwd activations received (fp32 [M,H]) go into slot x[0]
   int64_t step_index = 0;
   // stats
@@ -504,6 +524,27 @@ class Executor {
     // memory tier: the device's memory_gib caps the rank (cost_model.cpp:130-153
     // applies the same per-device budget to its layer-memory estimate)
     const double cap = L.cluster.devices[size_t(role.device)].memory_gib * double(1ull << 30);
+    // weight-gradient grouping: as many micro-batches per group as fit
+    wg_ = 1;
+    wg_nbuf_ = n_slots > 1 ? 2 : 1;
+    if (cfg.wgrad_group != 0 && cfg.wgrad_group != 1 && !cfg.recompute && role.n_mb > 1) {
+      double budget = cap - double(arena.total() + tp_exchange_bytes()) - double(12ull << 30);
+      if (!cfg.validate_only) {
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess)
+          budget = std::min(budget, double(fr) - double(arena.total() + tp_exchange_bytes()) -
+                                        double(6ull << 30));
+      }
+      const int64_t want = cfg.wgrad_group > 1 ? std::min<int64_t>(cfg.wgrad_group, role.n_mb)
+                                               : role.n_mb;
+      const int64_t fit = budget > 0 ? int64_t(budget / double(wg_nbuf_ * wg_bytes_per_mb())) : 0;
+      int64_t G = std::min(want, fit);
+      if (wg_nbuf_ == 2 && G < n_slots - 1) G = 1;
+      if (G >= 2) {
+        wg_ = G;
+        arena.reserve(size_t(wg_nbuf_ * wg_ * wg_bytes_per_mb()) + size_t(wg_nbuf_) * 4096 * 10);
+      }
+    }
     if (double(arena.total() + tp_exchange_bytes()) > cap)
       throw Infeasible("plan does not fit device '" + L.cluster.devices[size_t(role.device)].id +
                        "': rank needs " + std::to_string((arena.total() + tp_exchange_bytes()) >> 20) +
@@ -565,6 +606,29 @@ class Executor {
     if (role.last_stage) {
       logits = arena.take<float>(M * Vr);
       ce_scr = arena.take<float>(6 * M);
+    }
+    if (wg_ > 1) {
+      const int64_t R = wg_ * M;  // token rows per group buffer
+      wst_.assign(size_t(wg_nbuf_ * nl), WStash{});
+      wst_xf_.assign(size_t(wg_nbuf_), nullptr);
+      wst_dlog_.assign(size_t(wg_nbuf_), nullptr);
+      for (int64_t b = 0; b < wg_nbuf_; ++b) {
+        for (int64_t l = 0; l < nl; ++l) {
+          WStash& w = wst_[size_t(b * nl + l)];
+          w.act = arena.take<bf16>(R * F);
+          w.hn = arena.take<bf16>(R * H);
+          w.attn = arena.take<bf16>(R * kr);
+          w.xn = arena.take<bf16>(R * H);
+          w.dxob = arena.take<bf16>(R * H);
+          w.dgu = arena.take<bf16>(R * 2 * F);
+          w.dxmb = arena.take<bf16>(R * H);
+          w.dqkv = arena.take<bf16>(R * qkvw);
+        }
+        if (role.last_stage) {
+          wst_xf_[size_t(b)] = arena.take<bf16>(R * H);
+          wst_dlog_[size_t(b)] = arena.take<bf16>(R * Vr);
+        }
+      }
     }
     loss_acc = arena.take<float>(32);
     sp_ = reinterpret_cast<StepParams*>(loss_acc + 16);
@@ -941,6 +1005,13 @@ class Executor {
   void layer_fwd(Slot& sl, int64_t l, bool recompute = false) {
     LayerActs& a = acts(sl, l);
     const LayerW& w = lw[size_t(l)];
+    if (wg_ > 1) {
+      WStash& st = ws(l, cur_mb_);
+      a.xn = wrow(st.xn, cur_mb_, H);
+      a.hn = wrow(st.hn, cur_mb_, H);
+      a.attn = wrow(st.attn, cur_mb_, kr);
+      a.act = wrow(st.act, cur_mb_, F);
+    }
     float* x_in = sl.x[size_t(l)];
     float* x_out = sl.x[size_t(l + 1)];
     const float eps = float(L.model.norm_eps);
@@ -1054,6 +1125,11 @@ class Executor {
 
   void head_fwd(Slot& sl, int64_t mbi) {
     const float eps = float(L.model.norm_eps);
+    if (wg_ > 1) {
+      const size_t b = size_t((mbi / wg_) % wg_nbuf_);
+      sl.xf = wrow(wst_xf_[b], mbi, H);
+      sl.dlogits = wrow(wst_dlog_[b], mbi, Vr);
+    }
     k_rmsnorm_fwd(sl.x[size_t(nl)], nullptr, nullptr, final_norm.p32, sl.xf, sl.rstdf, int(M), int(H), eps, stream);
     kcheck("rmsnorm_fwd");
     gemm_kind_ = 2;
@@ -1099,25 +1175,36 @@ class Executor {
     LayerActs& a = acts(sl, l);
     const LayerW& w = lw[size_t(l)];
     const bool first_mb = accum_first_;
+    // weight-gradient GEMM operands: this micro-batch's rows (K = M), or with
+    // grouping the group's token-concatenated rows at its last micro-batch
+    const int64_t mbi = cur_mb_;
+    const bool grouped = wg_ > 1;
+    const bool do_wgrad = !grouped || wg_end(mbi);
+    const int64_t Kw = grouped ? (mbi % wg_ + 1) * M : M;
+    const int wbeta = grouped ? (mbi / wg_ > 0 ? 1 : 0) : (first_mb ? 0 : 1);
+    WStash* st = grouped ? &ws(l, mbi) : nullptr;
+    bf16* dgu_ = grouped ? wrow(st->dgu, mbi, 2 * F) : dgu;
+    bf16* dqkv_saved = dqkv;
+    if (grouped) dqkv = wrow(st->dqkv, mbi, qkvw);
+    auto wgemm = [&](int64_t Mo, const bf16* Ag, int64_t lda_, const bf16* Bg, int64_t ldb_,
+                     float* G) {
+      GemmDesc g = g2(Mo, H, Kw, Ag, 1, lda_, Bg, 1, ldb_, G, H, 1);
+      g.beta = wbeta;
+      gemm(g);
+    };
     // MLP: down projection
     gemm(g2(M, F, H, dxob, 0, H, w.wdown.p16, 0, H, da, F, 0));
-    {
-      GemmDesc g = g2(F, H, M, a.act, 1, F, dxob, 1, H, w.wdown.g32, H, 1);
-      g.beta = first_mb ? 0 : 1;
-      gemm(g);
-    }
-    k_swiglu_bwd(a.gu, da, dgu, int(M), int(F), stream);
+    if (do_wgrad)
+      wgemm(F, grouped ? st->act : a.act, F, grouped ? st->dxob : dxob, H, w.wdown.g32);
+    k_swiglu_bwd(a.gu, da, dgu_, int(M), int(F), stream);
     kcheck("swiglu_bwd");
     const bf16* dyr = dy16;
     if (tp_peer_)
-      dyr = tp_partial_gemm(g2(M, H, 2 * F, dgu, 0, 2 * F, w.wgu.p16, 1, H, nullptr, H, 0));
+      dyr = tp_partial_gemm(g2(M, H, 2 * F, dgu_, 0, 2 * F, w.wgu.p16, 1, H, nullptr, H, 0));
     else
-      gemm(g2(M, H, 2 * F, dgu, 0, 2 * F, w.wgu.p16, 1, H, dy16, H, 0));
-    {
-      GemmDesc g = g2(2 * F, H, M, dgu, 1, 2 * F, a.hn, 1, H, w.wgu.g32, H, 1);
-      g.beta = first_mb ? 0 : 1;
-      gemm(g);
-    }
+      gemm(g2(M, H, 2 * F, dgu_, 0, 2 * F, w.wgu.p16, 1, H, dy16, H, 0));
+    if (do_wgrad)
+      wgemm(2 * F, grouped ? st->dgu : dgu_, 2 * F, grouped ? st->hn : a.hn, H, w.wgu.g32);
     if (tp_peer_)
       tp_sync();
     else
@@ -1126,17 +1213,14 @@ class Executor {
     const int64_t ys = int64_t(tp_slot_elems());
     // dx_mid = dx_out + rmsnorm_bwd(dhn);  (reuse dxi as dx_mid storage)
     float* dxm = dxi;
-    bf16* dxmb = dxib;
+    bf16* dxmb = grouped ? wrow(st->dxmb, mbi, H) : dxib;
     k_rmsnorm_bwd(dyr, nullptr, a.x_mid, a.rstd2, w.mlp_norm.p32, dxo, dxm, dxmb, w.mlp_norm.g32,
                   int(M), int(H), dg_part_, stream, ny, ys);
     kcheck("rmsnorm_bwd");
     // attention: O projection
     gemm(g2(M, kr, H, dxmb, 0, H, w.wo.p16, 0, H, dattn, kr, 0));
-    {
-      GemmDesc g = g2(kr, H, M, a.attn, 1, kr, dxmb, 1, H, w.wo.g32, H, 1);
-      g.beta = first_mb ? 0 : 1;
-      gemm(g);
-    }
+    if (do_wgrad)
+      wgemm(kr, grouped ? st->attn : a.attn, kr, grouped ? st->dxmb : dxmb, H, w.wo.g32);
     attention_bwd(a);
     k_rope(dqkv, int(M), int(S), int(nh), int(d), float(L.model.rope_theta), 1, stream);
     kcheck("rope");
@@ -1144,11 +1228,8 @@ class Executor {
       dyr = tp_partial_gemm(g2(M, H, qkvw, dqkv, 0, qkvw, w.wqkv.p16, 1, H, nullptr, H, 0));
     else
       gemm(g2(M, H, qkvw, dqkv, 0, qkvw, w.wqkv.p16, 1, H, dy16, H, 0));
-    {
-      GemmDesc g = g2(qkvw, H, M, dqkv, 1, qkvw, a.xn, 1, H, w.wqkv.g32, H, 1);
-      g.beta = first_mb ? 0 : 1;
-      gemm(g);
-    }
+    if (do_wgrad)
+      wgemm(qkvw, grouped ? st->dqkv : dqkv, qkvw, grouped ? st->xn : a.xn, H, w.wqkv.g32);
     if (tp_peer_)
       tp_sync();
     else
@@ -1157,6 +1238,7 @@ class Executor {
     k_rmsnorm_bwd(dyr, nullptr, sl.x[size_t(l)], a.rstd1, w.attn_norm.p32, dxm, dxi, dxib,
                   w.attn_norm.g32, int(M), int(H), dg_part_, stream, ny, ys);
     kcheck("rmsnorm_bwd");
+    dqkv = dqkv_saved;
   }
 
   void attention_bwd(LayerActs& a) {
@@ -1241,6 +1323,8 @@ class Executor {
     float* cur = dx[0];
     float* nxt = dx[1];
     bf16* curb = dxb;
+    const bool grouped = wg_ > 1;
+    if (grouped && nl > 0) curb = wrow(ws(nl - 1, mbi).dxob, mbi, H);
     if (role.last_stage) {
       gemm_kind_ = 2;
       const bf16* dyr = dy16;
@@ -1248,9 +1332,17 @@ class Executor {
         dyr = tp_partial_gemm(g2(M, H, Vr, sl.dlogits, 0, Vr, lm_head.p16, 1, H, nullptr, H, 0));
       else
         gemm(g2(M, H, Vr, sl.dlogits, 0, Vr, lm_head.p16, 1, H, dy16, H, 0));
-      GemmDesc g = g2(Vr, H, M, sl.dlogits, 1, Vr, sl.xf, 1, H, lm_head.g32, H, 1);
-      g.beta = accum_first_ ? 0 : 1;
-      gemm(g);
+      if (!grouped) {
+        GemmDesc g = g2(Vr, H, M, sl.dlogits, 1, Vr, sl.xf, 1, H, lm_head.g32, H, 1);
+        g.beta = accum_first_ ? 0 : 1;
+        gemm(g);
+      } else if (wg_end(mbi)) {
+        const size_t b = size_t((mbi / wg_) % wg_nbuf_);
+        GemmDesc g = g2(Vr, H, (mbi % wg_ + 1) * M, wst_dlog_[b], 1, Vr, wst_xf_[b], 1, H,
+                        lm_head.g32, H, 1);
+        g.beta = mbi / wg_ > 0 ? 1 : 0;
+        gemm(g);
+      }
       gemm_kind_ = 0;
       if (tp_peer_)
         tp_sync();
@@ -1267,8 +1359,11 @@ class Executor {
       kcheck("cast_bf16");
     }
     for (int64_t l = nl - 1; l >= 0; --l) {
-      // dxi aliases the ping-pong partner; dxb reused in place (row-local ops)
-      layer_bwd(sl, l, cur, curb, nxt, curb);
+      // dxi aliases the ping-pong partner; dxb reused in place (row-local ops);
+      // with wgrad grouping the bf16 input grad lands in layer l-1's stash row
+      bf16* nb = (grouped && l > 0) ? wrow(ws(l - 1, mbi).dxob, mbi, H) : (grouped ? dxb : curb);
+      layer_bwd(sl, l, cur, curb, nxt, nb);
+      curb = nb;
       std::swap(cur, nxt);
       group_ready(int(role.layer_start + l));
     }
@@ -1677,6 +1772,8 @@ class Executor {
     j["sm_total"] = sm_total;
     j["sm_applied"] = sm_applied;
     j["sm_cap_mode"] = sm_mode;
+    j["wgrad_group"] = wg_;
+    j["wgrad_group_buffers"] = wg_nbuf_;
     j["tp_reduce"] = tp_peer_ ? (tp_crit_ >= 0 ? "peer(pull from tp rank " + std::to_string(tp_crit_) + ")" : std::string("peer(push)")) : (role.tp > 1 ? std::string("nccl") : std::string("none"));
     j["sm_fraction"] = role.sm_fraction;
     j["arena_bytes"] = arena.total();

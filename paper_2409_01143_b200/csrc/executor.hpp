@@ -20,6 +20,13 @@ struct ExecConfig {
   bool profile_gemm = false;          // per-GEMM CUDA events (roofline evidence); eager
   bool graph_gemm_events = false;     // per-GEMM CUDA events inside the step graph
   bool fuse_swiglu = true;            // SwiGLU in the gate-up GEMM epilogue
+  // weight-gradient GEMMs over G token-concatenated micro-batches: -1 = auto
+  // (all micro-batches that fit in memory), 0/1 = per micro-batch, G = force.
+  // Off by default: +18-20 % wgrad throughput in isolation
+  // (scripts/bench_wgrad_concat.py), but a full-SM B200 is power-capped and
+  // the step time stayed flat (100.9 vs 101.0 ms, the clock dropped
+  // 1507 -> 1372 MHz) while the stash costs 9-90 GiB per rank
+  int wgrad_group = 1;
   bool cuda_graph = true;             // replay the captured step graph (after step 0)
   std::string attention = "fused";    // "fused" (flash, tcgen05) | "unfused" (GEMM+softmax)
   bool dp_overlap = true;             // DP sync + AdamW per layer on a second stream

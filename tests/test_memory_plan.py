@@ -52,13 +52,17 @@ def test_recompute_shrinks_activation_memory_and_memory_gib_caps():
     m = open(os.path.join(CFG, "models", e["model"] + ".json")).read()
     p = open(os.path.join(CFG, "plans", name + ".json")).read()
     world = len(c["devices"])
-    full = _dry(json.dumps(c), m, p, {}, world)
+    # stored activations without weight-gradient grouping (auto grouping only
+    # takes memory that is left over, so it never makes a plan infeasible)
+    full = _dry(json.dumps(c), m, p, {"wgrad_group": 1}, world)
     rc = _dry(json.dumps(c), m, p, {"recompute": True}, world)
     assert rc < 0.9 * full, (rc / 2**30, full / 2**30)
     cap_gib = (rc + full) / 2 / 2**30
     for d in c["devices"]:
         d["memory_gib"] = cap_gib
     with pytest.raises(HexexecError) as ei:
-        _dry(json.dumps(c), m, p, {}, world)
+        _dry(json.dumps(c), m, p, {"wgrad_group": 1}, world)
     assert "memory_gib" in str(ei.value)
+    with pytest.raises(HexexecError):
+        _dry(json.dumps(c), m, p, {"wgrad_group": -1}, world)
     assert _dry(json.dumps(c), m, p, {"recompute": True}, world) == rc
