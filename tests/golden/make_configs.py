@@ -82,6 +82,14 @@ MODELS = {
                  "num_heads": 40, "ffn_dim": 13824, "vocab_size": 32000},
     "llama30b": {"num_layers": 60, "hidden_dim": 6656, "seq_len": 2048, "bytes_per_element": 2,
                  "num_heads": 52, "ffn_dim": 17920, "vocab_size": 32000},
+    # 2-layer, short-sequence cuts of the 13B / 30B layer shapes (GPU sharding-
+    # invariance tests of the H = 5120 / 6656, 40 / 52-head, F = 13824 / 17920 paths)
+    "llama13b_2l_s256": {"num_layers": 2, "hidden_dim": 5120, "seq_len": 256,
+                         "bytes_per_element": 2, "num_heads": 40, "ffn_dim": 13824,
+                         "vocab_size": 1024},
+    "llama30b_2l_s256": {"num_layers": 2, "hidden_dim": 6656, "seq_len": 256,
+                         "bytes_per_element": 2, "num_heads": 52, "ffn_dim": 17920,
+                         "vocab_size": 1024},
 }
 
 
@@ -136,6 +144,12 @@ HAND = {
     "llama7b_4_mix": ("b200_4_tiers_cal", "llama7b", plan([
         pipe(20, 1, [stage(["g0"], 0, 16), stage(["g1"], 16, 16)]),
         pipe(12, 1, [stage(["g2", "g3"], 0, 32)])], 32)),
+    "llama13b_2l_1gpu": ("b200_1", "llama13b_2l_s256", plan([pipe(2, 1, [stage(["g0"], 0, 2)])], 2)),
+    "llama13b_2l_tp31": ("b200_2_capped", "llama13b_2l_s256",
+                         plan([pipe(2, 1, [stage(["g0", "g1"], 0, 2, [3, 1])])], 2)),
+    "llama30b_2l_1gpu": ("b200_1", "llama30b_2l_s256", plan([pipe(2, 1, [stage(["g0"], 0, 2)])], 2)),
+    "llama30b_2l_tp31": ("b200_2_capped", "llama30b_2l_s256",
+                         plan([pipe(2, 1, [stage(["g0", "g1"], 0, 2, [3, 1])])], 2)),
     # cfg2 with widths from the calibrated speeds (1270 : 525 ~ 5 : 2)
     "llama7b_4l_tp52": ("b200_2_capped", "llama7b_4l",
                         plan([pipe(8, 1, [stage(["g0", "g1"], 0, 4, [5, 2])])], 4)),

@@ -5,6 +5,7 @@ Runs `steps` training steps of configs/plans/<name>.json and saves, per rank,
 the loss and every held tensor's reduced gradient and updated weights (after
 the first step) to <out>/rank<r>.npz."""
 import json
+import re
 import os
 import sys
 
@@ -33,7 +34,10 @@ def main():
         tok = ex.synth_tokens(s) if (host_tokens and ex.role["active"]) else None
         losses.append(ex.step(tok))
         if s == 0 and ex.role["active"]:
+            only = os.environ.get("HEXEXEC_TEST_READ")  # regex: read only these tensors
             for t in ex.role["tensors"]:
+                if only and not re.search(only, t["name"]):
+                    continue
                 res[t["name"] + "|grad"] = ex.read(t["name"], 1)
                 res[t["name"] + "|w"] = ex.read(t["name"], 0)
                 res[t["name"] + "|row0"] = np.int64(t["row0"])
