@@ -146,6 +146,8 @@ hexexec_status hexexec_k_gemm_peers(void* const* peers, int n);
 /* tile raster of every later GEMM (process-wide): bands of group_m M-tiles
  * walked M-fastest (default 8); 0 = N-fastest (tuning / microbenchmarks) */
 hexexec_status hexexec_k_gemm_raster(int group_m);
+/* SMs the persistent GEMM grid of later launches may occupy (0 = all) */
+hexexec_status hexexec_k_gemm_sm_limit(int sms);
 /* fused causal attention over the head-interleaved QKV buffer [mb*S, nh*3*d]:
  * out [mb*S, nh*d] bf16, lse [mb*nh, S] (log2 domain); backward writes
  * dq/dk/dv into dqkv [mb*S, nh*3*d] (delta / dq_acc: fp32 scratch of

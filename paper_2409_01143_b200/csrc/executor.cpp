@@ -891,7 +891,11 @@ class Executor {
   int32_t* tok_of(int64_t mbi) { return tokens + mbi * mb * (S + 1); }
 
   // ------------------------------------------------------------ TP exchange
-  bool use_tp_peer() const { return role.tp > 1 && cfg.tp_reduce == "peer"; }
+  // (tp > kMaxGemmPeers + 1: the GEMM epilogue has no map for more peers; such
+  // stages reduce through NCCL)
+  bool use_tp_peer() const {
+    return role.tp > 1 && role.tp <= kMaxGemmPeers + 1 && cfg.tp_reduce == "peer";
+  }
   size_t tp_slot_elems() const { return size_t(M * H); }
   size_t tp_exchange_bytes() const {
     if (!use_tp_peer()) return 0;
@@ -902,7 +906,6 @@ class Executor {
   // the TP communicator, map every peer's buffer
   void setup_tp_exchange() {
     if (!use_tp_peer()) return;
-    if (role.tp > 4) throw LimitExceeded("tp_reduce=peer supports tp <= 4");
     ncclComm_t c = tp_comm();
     int me = 0, n = 0;
     HX_NCCL(ncclCommUserRank(c, &me));
