@@ -81,6 +81,7 @@ ExecConfig parse_exec_config(const std::string& text) {
       else if (k == "graph_gemm_events") c.graph_gemm_events = v.get<bool>();
       else if (k == "fuse_swiglu") c.fuse_swiglu = v.get<bool>();
       else if (k == "wgrad_group") c.wgrad_group = v.get<int>();
+      else if (k == "pdl") c.pdl = v.get<bool>();
       else throw ParseError("exec config: unknown key '" + k + "'");
     } catch (const nlohmann::json::exception& e) {
       throw ParseError("exec config: bad value for '" + k + "'");
@@ -360,6 +361,7 @@ class Executor {
     HX_CUDA(cudaSetDevice(dev));
     HX_CUDA(cudaDeviceGetAttribute(&sm_total, cudaDevAttrMultiProcessorCount, dev));
     setup_stream();
+    gemm_set_pdl(cfg.pdl ? 1 : 0);
     for (auto& e : ev_eager_) HX_CUDA(cudaEventCreate(&e));
     for (auto& e : ev_graph_) HX_CUDA(cudaEventCreate(&e));
     for (auto& e : tmr_) HX_CUDA(cudaEventCreate(&e));

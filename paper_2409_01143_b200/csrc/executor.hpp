@@ -27,6 +27,10 @@ struct ExecConfig {
   // the step time stayed flat (100.9 vs 101.0 ms, the clock dropped
   // 1507 -> 1372 MHz) while the stash costs 9-90 GiB per rank
   int wgrad_group = 1;
+  // programmatic dependent launch of the GEMMs (prologue overlaps the
+  // previous kernel's tail); off: no measurable change on the power-capped
+  // step (100.9-101.2 ms either way)
+  bool pdl = false;
   bool cuda_graph = true;             // replay the captured step graph (after step 0)
   std::string attention = "fused";    // "fused" (flash, tcgen05) | "unfused" (GEMM+softmax)
   bool dp_overlap = true;             // DP sync + AdamW per layer on a second stream

@@ -82,5 +82,7 @@ void gemm_set_sm_limit(int sms);
 void gemm_force_cta_group(int cg);
 // grouped tile raster: bands of g M-tiles (default 8); 0 = n fastest
 void gemm_set_group_m(int g);
+// programmatic dependent launch (griddepcontrol.wait after the prologue): 1 = on
+void gemm_set_pdl(int on);
 
 }  // namespace hexexec

@@ -236,6 +236,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
+  // programmatic dependent launch: everything above (barriers, TMEM, tensor-map
+  // prefetch) overlaps the previous kernel's tail; no global memory is touched
+  // before the previous grid has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0) {
     if (lane == 0) {
@@ -601,6 +605,7 @@ int g_sm_limit = 0;
 int g_num_sms = 0;
 int g_force_cg = 0;  // 0 = auto, 1 / 2 = force (tests)
 int g_group_m = 8;   // grouped raster band height in M-tiles (0 = n fastest)
+int g_pdl = 0;       // launch with programmatic stream serialization
 
 cudaError_t load_encode() {
   std::call_once(g_encode_once, [] {
@@ -679,13 +684,15 @@ cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = g_pdl ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mr, mw, pm, p);
 }
 
@@ -729,6 +736,7 @@ int choose_split(int T, int P, int kblocks, bool direct) {
 void gemm_set_sm_limit(int sms) { g_sm_limit = sms; }
 void gemm_force_cta_group(int cg) { g_force_cg = cg; }
 void gemm_set_group_m(int g) { g_group_m = std::max(0, g); }
+void gemm_set_pdl(int on) { g_pdl = on ? 1 : 0; }
 
 cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream) {
   cudaError_t e = load_encode();
