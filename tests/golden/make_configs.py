@@ -55,6 +55,7 @@ CLUSTERS = {
     "b200_8_tiers": cluster(TIERS8, {"tierF": ["g0", "g1", "g2", "g3"], "tierH": ["g4", "g5"],
                                      "tierT": ["g6", "g7"]}),
     "b200_8_even": cluster([(f"g{i}", F) for i in range(8)]),
+    "b200_4_ht": cluster([("g0", HALF), ("g1", HALF), ("g2", THIRD), ("g3", THIRD)]),
     # homogeneous clusters with the SAME aggregate compute as the capped ones
     # (the "even-split plan at equal aggregate compute" comparison)
     "b200_2_eq": cluster([(f"g{i}", (F + THIRD) / 2) for i in range(2)]),
@@ -150,6 +151,13 @@ HAND = {
     "llama30b_2l_1gpu": ("b200_1", "llama30b_2l_s256", plan([pipe(2, 1, [stage(["g0"], 0, 2)])], 2)),
     "llama30b_2l_tp31": ("b200_2_capped", "llama30b_2l_s256",
                          plan([pipe(2, 1, [stage(["g0", "g1"], 0, 2, [3, 1])])], 2)),
+    # the pipelines of the calibrated 8-GPU plan (llama7b_8_cal) run alone:
+    # P0 / P1 = PP 16/16 on two full B200s (21 samples); P2 = TP 2 on the half
+    # tier (20 layers) + TP 2 on the third tier (12 layers), 22 samples
+    "llama7b_cal_p0": ("b200_2_even", "llama7b", plan([
+        pipe(21, 1, [stage(["g0"], 0, 16), stage(["g1"], 16, 16)])], 32)),
+    "llama7b_cal_p2": ("b200_4_ht", "llama7b", plan([
+        pipe(22, 1, [stage(["g0", "g1"], 0, 20), stage(["g2", "g3"], 20, 12)])], 32)),
     # cfg2 with widths from the calibrated speeds (1270 : 525 ~ 5 : 2)
     "llama7b_4l_tp52": ("b200_2_capped", "llama7b_4l",
                         plan([pipe(8, 1, [stage(["g0", "g1"], 0, 4, [5, 2])])], 4)),
