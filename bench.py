@@ -378,7 +378,28 @@ def cpu_reference(name: str, samples: int, warmup: int) -> dict:
     _, ff = model_flops(md, S)
     t_full = statistics.median(times) * ff / f1
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    cores = cores or 1
+    # the reference's own CPU path for the plan (SURVEY 8(d) "CPU reference
+    # timing" (a)): hexplan_schedule on this config's cluster, compiled from the
+    # reference sources (oracle/_ref), HEXPLAN_THREADS = host cores
+    planner = None
+    try:
+        from oracle import refshim
+        _, _, _, idx = load(name)
+        if refshim.available():
+            kind = "symmetric" if idx["source"].endswith("symmetric") else "schedule"
+            if not idx.get("config"):  # hand plan: time the scheduler on its cluster
+                idx = dict(idx, config={"global_batch": json.loads(p)["global_batch"],
+                                        "iterations": 20, "seed": 0, "threads": cores})
+            t0 = time.perf_counter()
+            res = refshim.plan(c, m, json.dumps(idx["config"]), kind)
+            planner = {"hexplan": kind, "wall_s": round(time.perf_counter() - t0, 4),
+                       "found": bool(res.get("found")), "predicted_s": res.get("cost"),
+                       "config": idx["config"]}
+    except Exception as e:  # noqa: BLE001  (reported, never fatal for the bench)
+        planner = {"error": str(e)[:200]}
     return {"value": S / t_full, "unit": "tokens/s", "cores": cores, "kind": "port",
+            "reference_planner": planner,
             "sample": (f"numpy fp32 oracle (oracle/numeric.py), 1 sample x {S} tokens through "
                        f"embedding + 1 decoder layer + LM head/CE, fwd+bwd, median of {samples}, "
                        f"x{ff / f1:.2f} training-FLOP ratio to the {md['num_layers']}-layer model; "
@@ -432,7 +453,8 @@ def main():
                 / ref["value"] * 1e3,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic", "config": config,
-                "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                                     "reference_planner")},
                 "e2e": {"value": ref["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0},
                 "reference_cost_model": reference_cost(asym, None)}
@@ -474,7 +496,7 @@ def main():
     cpu = None
     if a.gpus == 1 and not a.no_cpu_baseline:
         cb = cpu_reference(asym, samples=1, warmup=0)
-        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "reference_planner")}
     line = {
         "metric": METRIC, "value": s["tokens_per_s"], "unit": "tokens/s", "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": s["ms_per_step"],
