@@ -148,6 +148,9 @@ hexexec_status hexexec_k_gemm_peers(void* const* peers, int n);
 hexexec_status hexexec_k_gemm_raster(int group_m);
 /* SMs the persistent GEMM grid of later launches may occupy (0 = all) */
 hexexec_status hexexec_k_gemm_sm_limit(int sms);
+/* A-tile multicast of later GEMMs: 2 = clusters of two CTA pairs along N
+ * sharing the A tile through TMA multicast, 1 = pairs only (default) */
+hexexec_status hexexec_k_gemm_multicast(int mc);
 /* fused causal attention over the head-interleaved QKV buffer [mb*S, nh*3*d]:
  * out [mb*S, nh*d] bf16, lse [mb*nh, S] (log2 domain); backward writes
  * dq/dk/dv into dqkv [mb*S, nh*3*d] (delta / dq_acc: fp32 scratch of

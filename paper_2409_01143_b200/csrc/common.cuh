@@ -201,6 +201,19 @@ HX_DEVICE void tma_load_4d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar,
       : "memory");
 }
 
+// the same, multicast to the CTAs of `mask` (same smem offset in each); every
+// destination's bytes are counted on its own pair leader's mbarrier
+HX_DEVICE void tma_load_4d_2sm_mc(void* dst, const CUtensorMap* map, uint64_t* bar, uint16_t mask,
+                                  int c0, int c1, int c2, int c3) {
+  const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "h"(mask)
+      : "memory");
+}
+
 template <uint32_t kCols>
 HX_DEVICE void tmem_alloc_2sm(uint32_t* slot) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(

@@ -84,5 +84,7 @@ void gemm_force_cta_group(int cg);
 void gemm_set_group_m(int g);
 // programmatic dependent launch (griddepcontrol.wait after the prologue): 1 = on
 void gemm_set_pdl(int on);
+// 2: A-tile TMA multicast across two CTA pairs along N (clusters of 4), 1: off
+void gemm_set_multicast(int mc);
 
 }  // namespace hexexec

@@ -50,6 +50,8 @@ struct EpiParams {
   int npeer;         // extra copies of every stored C tile (TP peers' buffers)
   int group_m;       // grouped tile raster (M-tiles per band), 0 = n fastest
   int act_mode;      // 1: SwiGLU epilogue, act = silu(g) * u to pm.m[0]
+  int mc;            // CTA pairs per cluster along N sharing the A tile (TMA multicast)
+  int n_tiles_c;     // cluster tiles along N = ceil(n_tiles / mc)
 };
 
 // TMA maps of the peer copies of C (IPC-mapped buffers of the other TP ranks,
@@ -136,11 +138,11 @@ HX_DEVICE void fence_proxy_async_global() {
 // M-tile: 8x the B bytes at M = 2048).  group_m = 0: n fastest.
 template <int TM>
 HX_DEVICE void decode_tile(const EpiParams& p, int t, int& m0, int& nt, int& z1, int& z2) {
-  const int per_batch = p.m_tiles * p.n_tiles;
+  const int per_batch = p.m_tiles * p.n_tiles_c;
   const int z = t / per_batch;
   const int r = t - z * per_batch;
   if (p.group_m > 0) {
-    const int per_group = p.group_m * p.n_tiles;
+    const int per_group = p.group_m * p.n_tiles_c;
     const int g = r / per_group;
     const int first = g * p.group_m;
     const int gm = min(p.group_m, p.m_tiles - first);
@@ -148,8 +150,8 @@ HX_DEVICE void decode_tile(const EpiParams& p, int t, int& m0, int& nt, int& z1,
     m0 = (first + q % gm) * TM;
     nt = q / gm;
   } else {
-    nt = r % p.n_tiles;
-    m0 = (r / p.n_tiles) * TM;
+    nt = r % p.n_tiles_c;
+    m0 = (r / p.n_tiles_c) * TM;
   }
   z1 = z % p.nb1;
   z2 = z / p.nb1;
@@ -199,18 +201,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;
+  // cluster = mc CTA pairs along N (pair q owns n-tile mc*nt_c + q); the pair's
+  // CTAs are cluster ranks 2q (leader) and 2q+1
+  const uint32_t crank_cl = CG == 2 ? cluster_ctarank() : 0;
+  const uint32_t crank = crank_cl & 1u;
+  const int pair_cl = int(crank_cl >> 1);
   const bool leader = crank == 0;
-  // pair index and pair count (persistent loop over pair tiles)
-  const int pid = blockIdx.x / CG;
-  const int npairs = gridDim.x / CG;
+  // cluster index and count (persistent loop over cluster tiles)
+  const int pid = blockIdx.x / (CG * p.mc);
+  const int npairs = gridDim.x / (CG * p.mc);
 
   if (threadIdx.x == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     for (int i = 0; i < ST; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], p.mc);  // one MMA commit per pair reading the stage
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -251,6 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         decode_unit(p, u, t, part);
         int m0, nt, z1, z2;
         decode_tile<TM>(p, t, m0, nt, z1, z2);
+        nt = nt * p.mc + pair_cl;
         int n0 = nt * BN;
         if (tile_skipped<TM>(p, m0, n0)) continue;
         int kb0, kb1;
@@ -264,7 +271,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* b = sB + stage * C::B_BYTES;
           int k0 = kb * BK;
           if (CG == 2) {
-            if (A_MN) {
+            if (p.mc == 2) {
+              // the A half of this CTA is the same for both pairs: pair 0 loads it
+              // into both (multicast), the bytes counted on each pair's leader
+              if (pair_cl == 0) {
+                const uint16_t mask = uint16_t((1u << crank_cl) | (1u << (crank_cl + 2)));
+                if (A_MN) {
+#pragma unroll
+                  for (int c = 0; c < BM / 64; ++c)
+                    tma_load_4d_2sm_mc(a + c * (BK * 128), &tmA, &full[stage], mask, am + c * 64,
+                                       k0, z1, z2);
+                } else {
+                  tma_load_4d_2sm_mc(a, &tmA, &full[stage], mask, k0, am, z1, z2);
+                }
+              }
+            } else if (A_MN) {
 #pragma unroll
               for (int c = 0; c < BM / 64; ++c)
                 tma_load_4d_2sm(a + c * (BK * 128), &tmA, &full[stage], am + c * 64, k0, z1, z2);
@@ -316,6 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         decode_unit(p, u, t, part);
         int m0, nt, z1, z2;
         decode_tile<TM>(p, t, m0, nt, z1, z2);
+        nt = nt * p.mc + pair_cl;
         int n0 = nt * BN;
         if (tile_skipped<TM>(p, m0, n0)) continue;
         int kb0, kb1;
@@ -340,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               tc_mma_f16(dtm, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
           }
           if (CG == 2)
-            tc_commit_2sm_mc(&empty[stage], 0x3);
+            tc_commit_2sm_mc(&empty[stage], p.mc == 2 ? uint16_t(0xF) : uint16_t(0x3));
           else
             tc_commit(&empty[stage]);
           if (++stage == ST) {
@@ -349,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         if (CG == 2)
-          tc_commit_2sm_mc(&tfull[acc], 0x3);
+          tc_commit_2sm_mc(&tfull[acc], uint16_t(0x3u << (2 * pair_cl)));
         else
           tc_commit(&tfull[acc]);
         if (++acc == 2) {
@@ -373,6 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       decode_unit(p, u, t, part);
       int m0, nt, z1, z2;
       decode_tile<TM>(p, t, m0, nt, z1, z2);
+      nt = nt * p.mc + pair_cl;
       int n0 = nt * BN;
       if (tile_skipped<TM>(p, m0, n0)) continue;
       int kb0, kb1;
@@ -483,7 +506,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) {
         if (CG == 2)
-          mbar_arrive_cluster(&tempty[acc], 0);  // the leader's MMA waits on both CTAs
+          mbar_arrive_cluster(&tempty[acc], crank_cl & ~1u);  // the pair leader's MMA waits on both CTAs
         else
           mbar_arrive(&tempty[acc]);
       }
@@ -606,6 +629,7 @@ int g_num_sms = 0;
 int g_force_cg = 0;  // 0 = auto, 1 / 2 = force (tests)
 int g_group_m = 8;   // grouped raster band height in M-tiles (0 = n fastest)
 int g_pdl = 0;       // launch with programmatic stream serialization
+int g_mc = 1;        // 2: A-tile multicast across two CTA pairs (clusters of 4)
 
 cudaError_t load_encode() {
   std::call_once(g_encode_once, [] {
@@ -679,6 +703,28 @@ cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
     attr_done = true;
   }
   if (grid <= 0) return cudaSuccess;
+  if (p.mc == 2) {
+    // clusters of 4 co-resident at once (GPC packing): one persistent wave
+    static int max_cl = 0;
+    if (max_cl == 0) {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(4 * 64);
+      q.blockDim = dim3(kThreads);
+      q.dynamicSmemBytes = C::SMEM;
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = 4;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = 1;
+      q.attrs = qa;
+      q.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &q) != cudaSuccess || n <= 0) n = 1;
+      max_cl = n;
+    }
+    const int lim = g_sm_limit > 0 ? std::max(1, g_sm_limit / 4) : max_cl;
+    grid = std::min(p.num_units, std::min(max_cl, lim)) * 4;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -686,7 +732,7 @@ cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.x = CG * p.mc;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -737,6 +783,7 @@ void gemm_set_sm_limit(int sms) { g_sm_limit = sms; }
 void gemm_force_cta_group(int cg) { g_force_cg = cg; }
 void gemm_set_group_m(int g) { g_group_m = std::max(0, g); }
 void gemm_set_pdl(int on) { g_pdl = on ? 1 : 0; }
+void gemm_set_multicast(int mc) { g_mc = mc == 2 ? 2 : 1; }
 
 cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream) {
   cudaError_t e = load_encode();
@@ -780,6 +827,10 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream) {
   p.n_tiles = (d.N + BN - 1) / BN;
   p.num_tiles = p.m_tiles * p.n_tiles * d.nb1 * d.nb2;
   p.group_m = d.causal == kCausalNone ? std::min(p.m_tiles, g_group_m) : 0;
+  // A multicast over two CTA pairs along N (dense, paired, >= 2 N tiles)
+  p.mc = (g_mc == 2 && CG == 2 && d.causal == kCausalNone && p.n_tiles >= 2) ? 2 : 1;
+  p.n_tiles_c = (p.n_tiles + p.mc - 1) / p.mc;
+  p.num_tiles = p.m_tiles * p.n_tiles_c * d.nb1 * d.nb2;
   if (d.beta && !d.c_fp32) return cudaErrorInvalidValue;
   CUtensorMap mc, mr;
   if (!make_map_c(&mc, d.C, d.c_fp32, d.N, d.M, d.ldc, d.cbs1, d.cbs2, d.nb1, d.nb2))
@@ -814,7 +865,8 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream) {
   p.ws = d.ws;
   p.ws_cnt = d.ws_cnt;
   CUtensorMap mw = mc;
-  if (d.causal == kCausalNone && d.split != 0 && d.npeer == 0 && !d.act && p.num_tiles > 0) {
+  if (d.causal == kCausalNone && d.split != 0 && d.npeer == 0 && !d.act && p.mc == 1 &&
+      p.num_tiles > 0) {
     const int kblocks = (d.K + BK - 1) / BK;
     const bool direct = d.beta && !d.R;
     int s = d.split > 1 ? std::min(d.split, std::max(1, kblocks))
@@ -831,7 +883,7 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream) {
       p.split_direct = direct ? 1 : 0;
     }
   }
-  const int grid = std::min(p.num_units, P) * CG;
+  const int grid = std::min(p.num_units, p.mc == 2 ? P / 2 : P) * CG * p.mc;
   const int am = d.A.mn_major, bmj = d.B.mn_major;
   if (CG == 2) {
     if (BN == 256) return dispatch_major<256, 2>(am, bmj, ma, mb, mc, mr, mw, pm, p, grid, stream);

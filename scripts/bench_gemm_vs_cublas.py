@@ -69,11 +69,15 @@ def main():
         t_n = timed(ours)
         assert L.hexexec_k_gemm_raster(8) == 0
         t_o = timed(ours)
+        assert L.hexexec_k_gemm_multicast(2) == 0
+        t_m = timed(ours)
+        assert L.hexexec_k_gemm_multicast(1) == 0
         t_c = timed(cublas)
         print(json.dumps({"tag": tag, "M": M, "N": N, "K": K, "ours_us": round(t_o * 1e3, 1),
                           "cublas_us": round(t_c * 1e3, 1),
                           "ours_tflops": round(f / t_o / 1e9, 1),
                           "ours_nfastest_tflops": round(f / t_n / 1e9, 1),
+                          "ours_amulticast_tflops": round(f / t_m / 1e9, 1),
                           "cublas_tflops": round(f / t_c / 1e9, 1)}), flush=True)
 
 

@@ -324,3 +324,29 @@ def test_init_and_tokens_match_oracle(cuda):
     assert L.hexexec_k_tokens(_ptr(tok), ns, S, s0, 7, step, V, None) == 0
     torch.cuda.synchronize()
     assert np.array_equal(tok.cpu().numpy(), O.tokens(7, step, s0, ns, S, V))
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(512, 1024, 256), (256, 768, 192), (2048, 4096, 1024),
+                                   (384, 1280, 320)])
+def test_gemm_a_multicast(cuda, a_mn, b_mn, M, N, K):
+    """Clusters of two CTA pairs along N sharing the A tile via TMA multicast
+    (odd N-tile counts leave the second pair of the last cluster out of range)."""
+    L = _L()
+    assert L.hexexec_k_gemm_multicast(2) == 0
+    try:
+        g = torch.Generator(device="cuda").manual_seed(M + N * 3 + K)
+        A = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+        B = torch.randn(N, K, device=cuda, generator=g).bfloat16()
+        ref = A.float() @ B.float().T
+        As = A.T.contiguous() if a_mn else A
+        Bs = B.T.contiguous() if b_mn else B
+        C16 = torch.zeros(M, N, device=cuda, dtype=torch.bfloat16)
+        _gemm(As, a_mn, Bs, b_mn, M, N, K, C16)
+        assert _rel(C16, ref) < 1e-2
+        C32 = torch.randn(M, N, device=cuda)
+        ref2 = C32 + ref
+        _gemm(As, a_mn, Bs, b_mn, M, N, K, C32, beta=1)
+        assert _rel(C32, ref2) < 2e-3
+    finally:
+        assert L.hexexec_k_gemm_multicast(1) == 0
