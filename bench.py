@@ -73,13 +73,22 @@ def load(name):
     return c, m, p, idx
 
 
+def full_model(c: str, m: str, p: str) -> dict:
+    """The model document with the executor's defaults filled in (num_heads,
+    ffn_dim, vocab_size, ...), from the product's own plan layout."""
+    from paper_2409_01143_b200.hexexec import Plan
+    pl = Plan(c, m, p)
+    try:
+        return pl.layout()["model"]
+    finally:
+        pl.close()
+
+
 def model_flops(m: dict, tokens: int) -> tuple[float, float]:
     """(reference-convention FLOPs, exact causal Llama training FLOPs) for
     `tokens` trained tokens.  Reference: 72*S*H^2*(1+S/6H) per token per layer
     (cost_model.cpp:17-21, :260-265).  Exact: 3x forward GEMM flops incl. the
     causal attention products and the LM head."""
-    from oracle import bookkeeping as bk
-    m = bk.model_defaults(m)
     L, H, S, F, V = m["num_layers"], m["hidden_dim"], m["seq_len"], m["ffn_dim"], m["vocab_size"]
     ref = 72.0 * S * H * H * (1 + S / (6.0 * H)) * L / S * tokens
     fwd = L * (2 * H * (4 * H + 3 * F) + 2 * S * H) + 2 * H * V
@@ -281,7 +290,8 @@ def summarize(r: dict, steps: int, pk: dict) -> dict:
     tokens = gb * S
     tps = tokens * steps / (r["dev_ms"] / 1e3)
     e2e = tokens * steps / (r["e2e_ms"] / 1e3)
-    ref_f, exact_f = model_flops(r["model"], tokens)
+    ref_f, exact_f = model_flops(full_model(json.dumps(r["cluster"]), json.dumps(r["model"]),
+                                            json.dumps(r["plan"])), tokens)
     step_s = r["dev_ms"] / 1e3 / steps
     # aggregate peak of the emulated tiers: sum over ranks of applied SM share x measured peak
     agg = r["sm_share"] * pk["bf16_tflops"] * 1e12
