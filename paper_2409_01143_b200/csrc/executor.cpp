@@ -82,6 +82,7 @@ ExecConfig parse_exec_config(const std::string& text) {
       else if (k == "fuse_swiglu") c.fuse_swiglu = v.get<bool>();
       else if (k == "wgrad_group") c.wgrad_group = v.get<int>();
       else if (k == "pdl") c.pdl = v.get<bool>();
+      else if (k == "tp_pull") c.tp_pull = v.get<std::string>();
       else throw ParseError("exec config: unknown key '" + k + "'");
     } catch (const nlohmann::json::exception& e) {
       throw ParseError("exec config: bad value for '" + k + "'");
@@ -97,6 +98,8 @@ ExecConfig parse_exec_config(const std::string& text) {
     throw ParseError("exec config: pp_protocol must be direct|leader");
   if (c.tp_reduce != "peer" && c.tp_reduce != "nccl")
     throw ParseError("exec config: tp_reduce must be peer|nccl");
+  if (c.tp_pull != "sm" && c.tp_pull != "ce")
+    throw ParseError("exec config: tp_pull must be sm|ce");
   if (c.tp_direction != "auto" && c.tp_direction != "push")
     throw ParseError("exec config: tp_direction must be auto|push");
   return c;
@@ -995,8 +998,14 @@ class Executor {
     k_tp_sync(tpp_, sp_, xop_++, stream);
     kcheck("tp_sync");
     if (tp_crit_ >= 0 && tpp_.me != tp_crit_ && !pad_) {
-      HX_CUDA(cudaMemcpyAsync(xslot(tpp_.me, b, tp_crit_), xslot(tp_crit_, b, tp_crit_),
-                              tp_slot_elems() * 2, cudaMemcpyDeviceToDevice, stream));
+      if (cfg.tp_pull == "ce") {
+        HX_CUDA(cudaMemcpyAsync(xslot(tpp_.me, b, tp_crit_), xslot(tp_crit_, b, tp_crit_),
+                                tp_slot_elems() * 2, cudaMemcpyDeviceToDevice, stream));
+      } else {
+        k_peer_copy(xslot(tpp_.me, b, tp_crit_), xslot(tp_crit_, b, tp_crit_),
+                    tp_slot_elems() * 2, sm_applied, stream);
+        kcheck("tp_pull");
+      }
       mark("tp_pull");
     }
   }

@@ -55,6 +55,10 @@ struct ExecConfig {
   // "auto": the critical rank of an uneven TP stage does not push (the others
   // pull its partial); "push": every rank pushes
   std::string tp_direction = "auto";
+  // how the faster ranks pull the critical rank's partial: "sm" = copy kernel
+  // with remote 16-byte loads, "ce" = copy-engine cudaMemcpyAsync; both ~400 GB/s
+  // (41 us per 16 MiB slot) and the same step time
+  std::string tp_pull = "ce";
 };
 
 ExecConfig parse_exec_config(const std::string& text);

@@ -785,6 +785,28 @@ void k_tp_sync(const TpPeers& p, const StepParams* sp, unsigned op, cudaStream_t
   tp_sync_kernel<<<1, 32, 0, s>>>(p, sp, op);
 }
 
+// copy of a peer's exchange slot into the local one (the pull of the critical
+// TP rank's partial): 16-byte remote loads over NVLink, 4 in flight per thread
+__global__ void __launch_bounds__(256) peer_copy_kernel(uint4* __restrict__ dst,
+                                                        const uint4* __restrict__ src, long long n16) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    uint4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = __ldcg(src + i + k * stride);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) dst[i + k * stride] = v[k];
+  }
+  for (; i < n16; i += stride) dst[i] = __ldcg(src + i);
+}
+void k_peer_copy(void* dst, const void* src, size_t bytes, int sms, cudaStream_t s) {
+  const long long n16 = (long long)(bytes / 16);
+  if (n16 > 0)
+    peer_copy_kernel<<<std::max(1, sms) * 4, 256, 0, s>>>(static_cast<uint4*>(dst),
+                                                          static_cast<const uint4*>(src), n16);
+}
+
 void k_step_tick(StepParams* sp, float b1, float b2, cudaStream_t s) {
   step_tick_kernel<<<1, 32, 0, s>>>(sp, b1, b2);
 }

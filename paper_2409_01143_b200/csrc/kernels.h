@@ -100,6 +100,8 @@ struct TpPeers {
   int tp, me;
 };
 void k_tp_sync(const TpPeers& p, const StepParams* sp, unsigned op, cudaStream_t s);
+// dst (local) <- src (peer memory), bytes % 16 == 0; grid of 4 CTAs per SM
+void k_peer_copy(void* dst, const void* src, size_t bytes, int sms, cudaStream_t s);
 
 // in-place rotary embedding of q and k inside the fused [M, nh*3*d] buffer
 // (rotate-half convention); inverse=1 applies the transpose (backward).
