@@ -48,6 +48,21 @@ HX_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// the same with a suspend-time hint (ns): the waiting warp may sleep until the
+// phase completes instead of re-polling (long waits: epilogue / producer)
+HX_DEVICE void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity), "r"(0x100000u)
+      : "memory");
+}
+
 // explicit shared-space vector loads (generic pointers into dynamic smem
 // otherwise compile to generic LD)
 HX_DEVICE float4 lds_f4(const void* p) {
