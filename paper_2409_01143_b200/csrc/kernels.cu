@@ -832,7 +832,10 @@ void k_embed_bwd(const int32_t* tok, const float* dx, float* dE, int M, int S, i
 void k_rmsnorm_fwd(const float* x, const bf16* y, float* xo, const float* g, bf16* out,
                    float* rstd, int M, int H, float eps, cudaStream_t s, int ny, long long ys) {
   if (M <= 0) return;
-  const int grid = std::min(M, 148 * 8);
+  // equal row counts per CTA within one resident wave (2048 rows: 1024 CTAs x 2
+  // rows rather than 1184 CTAs x 1-2 rows, whose 2-row CTAs form a tail)
+  const int per = (M + 148 * 8 - 1) / (148 * 8);
+  const int grid = (M + per - 1) / per;
   const int nc = (H + kNormChunk - 1) / kNormChunk;
 #define HX_NORM_FWD(NC) \
   rmsnorm_fwd_kernel<NC><<<grid, kNormThreads, 0, s>>>(x, y, xo, g, out, rstd, M, H, eps, ny, ys)
