@@ -151,6 +151,9 @@ hexexec_status hexexec_k_gemm_sm_limit(int sms);
 /* A-tile multicast of later GEMMs: 2 = clusters of two CTA pairs along N
  * sharing the A tile through TMA multicast, 1 = pairs only (default) */
 hexexec_status hexexec_k_gemm_multicast(int mc);
+/* 1: choose 128-wide output tiles where they quantise into fewer
+ * wave-equivalents than 256-wide ones; 0 (default): 256-wide whenever N >= 256 */
+hexexec_status hexexec_k_gemm_tile_auto(int on);
 /* fused causal attention over the head-interleaved QKV buffer [mb*S, nh*3*d]:
  * out [mb*S, nh*d] bf16, lse [mb*nh, S] (log2 domain); backward writes
  * dq/dk/dv into dqkv [mb*S, nh*3*d] (delta / dq_acc: fp32 scratch of

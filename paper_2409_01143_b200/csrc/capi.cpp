@@ -327,6 +327,11 @@ hexexec_status hexexec_k_gemm(int M, int N, int K, int nb1, int nb2, const void*
   return cuda_status(hexexec::gemm_bf16(d, as_stream(stream)));
 }
 
+hexexec_status hexexec_k_gemm_tile_auto(int on) {
+  hexexec::gemm_set_bn_auto(on);
+  return HEXEXEC_OK;
+}
+
 hexexec_status hexexec_k_gemm_multicast(int mc) {
   if (mc != 1 && mc != 2) return HEXEXEC_ERR_INVALID;
   hexexec::gemm_set_multicast(mc);

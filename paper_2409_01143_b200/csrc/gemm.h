@@ -86,5 +86,7 @@ void gemm_set_group_m(int g);
 void gemm_set_pdl(int on);
 // 2: A-tile TMA multicast across two CTA pairs along N (clusters of 4), 1: off
 void gemm_set_multicast(int mc);
+// 1: 128-wide tiles where they quantise into fewer wave-equivalents (default 0)
+void gemm_set_bn_auto(int on);
 
 }  // namespace hexexec
