@@ -1,0 +1,56 @@
+"""bench.py helpers (CPU): the nvidia-smi sampler keeps only rows inside the
+timed window and reports per-GPU medians, the delivered SM-GHz, and the
+reference-convention FLOP count (cost_model.cpp:17-21, :260-265)."""
+import datetime
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def test_clocks_window_and_per_gpu():
+    ck = bench.Clocks(2)
+    t0 = datetime.datetime(2026, 1, 1, 12, 0, 0)
+    rows = []
+    for i in range(10):
+        ts = (t0 + datetime.timedelta(milliseconds=100 * i)).strftime("%Y/%m/%d %H:%M:%S.%f")[:-3]
+        for g, mhz in (("0", 1500 + i), ("1", 1965)):
+            rows.append(f"{ts}, {g}, {mhz}, 1965, 900.0, 0x4, Not Active, Not Active, Not Active, "
+                        f"{'Active' if g == '0' else 'Not Active'}")
+    ck.f.write("\n".join(rows) + "\n")
+    ck.f.flush()
+    ck.p = type("P", (), {"terminate": lambda s: None, "wait": lambda s: 0})()
+    ck.t0 = t0 + datetime.timedelta(milliseconds=250)
+    ck.t1 = t0 + datetime.timedelta(milliseconds=750)
+    out = ck.stop()
+    assert out["samples"] == 10  # 5 timestamps x 2 GPUs inside the window
+    assert out["sm_mhz_per_gpu"] == {"0": 1505.0, "1": 1965.0}
+    assert out["reasons"] == ["sw_power_cap"]
+    assert out["gpu_of_rank"] == ["0", "1"]
+
+
+def test_sm_ghz_and_flops():
+    r = {"clocks": {"sm_mhz_per_gpu": {"0": 1500.0, "1": 1965.0}, "gpu_of_rank": ["0", "1"]},
+         "lin_per_rank": [[0, 0, 0, 1.0], [0, 0, 0, 56 / 148]]}
+    assert abs(bench.sm_ghz(r) - (148 * 1.5 + 56 * 1.965)) < 1e-9
+    c, m, p, _ = bench.load("llama7b_4l_1gpu")
+    md = bench.full_model(c, m, p)
+    ref, exact = bench.model_flops(md, 2048)
+    L, H, S = md["num_layers"], md["hidden_dim"], md["seq_len"]
+    assert abs(ref - 72.0 * 2048 * H * H * (1 + S / (6.0 * H)) * L) / ref < 1e-12
+    assert exact > ref  # exact counts the LM head and the non-causal-free GEMMs
+
+
+def test_default_plans_exist():
+    idx = json.load(open(os.path.join(ROOT, "configs", "index.json")))
+    for n, (asym, even) in bench.PLANS.items():
+        assert asym in idx
+        for e in (even or "").split(","):
+            assert not e or e in idx
+    for n, names in bench.ALT.items():
+        for a in names.split(","):
+            assert a in idx
