@@ -638,9 +638,9 @@ int g_force_cg = 0;  // 0 = auto, 1 / 2 = force (tests)
 int g_group_m = 8;   // grouped raster band height in M-tiles (0 = n fastest)
 int g_pdl = 0;       // launch with programmatic stream serialization
 int g_mc = 1;        // 2: A-tile multicast across two CTA pairs (clusters of 4)
-// pick 128-wide tiles when they quantise better: off -- measured, a 256 x 128
-// pair tile runs far below half a 256 x 256 one (2048x3072x4096: 794 vs 988
-// TFLOP/s; 2048x16512x4096: 877 vs 1218), the re-read A panel dominates
+// pick 128-wide tiles when they quantise better (off: only nearly empty waves
+// qualify, e.g. 2048 x 1024 outputs 645 vs 599 TFLOP/s; a 256 x 128 pair tile
+// takes 0.84 of a 256 x 256 one's time)
 int g_bn_auto = 0;
 
 cudaError_t load_encode() {
@@ -805,10 +805,9 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream) {
   if (d.R && !d.c_fp32) return cudaErrorInvalidValue;
   // CTA pairs when M fills 256 rows; tile width 256 for wide outputs, 128
   // otherwise -- or (g_bn_auto) when 128-wide tiles quantise into fewer
-  // wave-equivalents:
-  // cost = waves x tile time, a 128-wide tile at 0.54 of a 256-wide one (half
-  // the MMA work plus the re-read A panel), e.g. 2048 x 3072 outputs: 96 tiles
-  // = 2 waves on 74 pairs (65 % busy) vs 192 half tiles = 3 waves x 0.54
+  // wave-equivalents: cost = waves x tile time, a 256 x 128 pair tile measured
+  // at 0.84 of a 256 x 256 one (2048 x 3072 x 4096: 2 waves of 256-wide tiles
+  // 1012 TFLOP/s vs 3 waves of 128-wide 807; A multicast does not change it)
   int CG = d.M > 128 ? 2 : 1;
   if (g_force_cg) CG = g_force_cg;
   int BN = d.N >= 256 ? 256 : 128;
@@ -818,7 +817,7 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream) {
     const long long mt = (d.M + BM * CG - 1) / (BM * CG), z = (long long)d.nb1 * d.nb2;
     const long long t256 = mt * ((d.N + 255) / 256) * z, t128 = mt * ((d.N + 127) / 128) * z;
     const double c256 = double((t256 + slots - 1) / slots);
-    const double c128 = 0.54 * double((t128 + slots - 1) / slots);
+    const double c128 = 0.85 * double((t128 + slots - 1) / slots);
     if (c128 < 0.97 * c256) BN = 128;
   }
   const int BNC = BN / CG;

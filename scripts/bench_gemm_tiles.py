@@ -50,9 +50,11 @@ for tag, M, N, K, amn, bmn in CASES:
                                 B.data_ptr(), bmn, N if bmn else K, 0, 0, C.data_ptr(), N, 0, 0,
                                 0, 0, 1.0, 0, None) == 0
     out = {"tag": tag, "M": M, "N": N, "K": K}
-    for auto in (0, 1):
+    for auto, mc in ((0, 1), (1, 1), (1, 2)):
         L.hexexec_k_gemm_tile_auto(auto)
+        L.hexexec_k_gemm_multicast(mc)
         t = timed(go)
-        out[f"tflops_auto{auto}"] = round(2.0 * M * N * K / t / 1e9, 1)
+        out[f"tflops_auto{auto}_mc{mc}"] = round(2.0 * M * N * K / t / 1e9, 1)
+    L.hexexec_k_gemm_multicast(1)
     print(json.dumps(out), flush=True)
 L.hexexec_k_gemm_tile_auto(0)
