@@ -83,6 +83,7 @@ ExecConfig parse_exec_config(const std::string& text) {
       else if (k == "wgrad_group") c.wgrad_group = v.get<int>();
       else if (k == "pdl") c.pdl = v.get<bool>();
       else if (k == "tp_pull") c.tp_pull = v.get<std::string>();
+      else if (k == "fuse_rope") c.fuse_rope = v.get<bool>();
       else throw ParseError("exec config: unknown key '" + k + "'");
     } catch (const nlohmann::json::exception& e) {
       throw ParseError("exec config: bad value for '" + k + "'");
@@ -227,6 +228,7 @@ class Executor {
   size_t xflag_off_ = 0;
   unsigned xop_ = 0;
   bool tp_peer_ = false;
+  float2* rope_tab_ = nullptr;  // RoPE (cos, sin) [S][d/2] for the QKV epilogue
   int tp_crit_ = -1;  // TP index of the critical (slowest) rank, or -1
   // Weight-gradient grouping (wgrad_group): the operands of the four layer
   // weight-gradient GEMMs (and the LM head's) of G consecutive micro-batches
@@ -525,6 +527,7 @@ class Executor {
     arena.reserve(kGemmWsCounters * 4);
     arena.reserve(size_t(kRmsBwdCtas) * H * 4);             // rmsnorm bwd partial dg rows
     arena.reserve(M * 4);                                  // embedding bwd sort keys
+    arena.reserve(size_t(S) * size_t(d / 2) * 8);          // RoPE (cos, sin) table
     arena.reserve(role.batch * (S + 1) * 4);               // tokens
     // memory tier: the device's memory_gib caps the rank (cost_model.cpp:130-153
     // applies the same per-device budget to its layer-memory estimate)
@@ -599,6 +602,8 @@ class Executor {
     gemm_cnt_ = arena.take<int>(kGemmWsCounters);
     dg_part_ = arena.take<float>(size_t(kRmsBwdCtas) * H);
     embed_keys_ = arena.take<uint32_t>(M);
+    rope_tab_ = arena.take<float2>(S * (d / 2));
+    k_rope_table(rope_tab_, int(S), int(d), float(L.model.rope_theta), stream);
     ypart = arena.take<bf16>(M * H);
     da = arena.take<bf16>(M * F);
     dgu = arena.take<bf16>(M * 2 * F);
@@ -1032,9 +1037,21 @@ class Executor {
     // attention block
     k_rmsnorm_fwd(x_in, nullptr, nullptr, w.attn_norm.p32, a.xn, a.rstd1, int(M), int(H), eps, stream);
     kcheck("rmsnorm_fwd");
-    gemm(g2(M, qkvw, H, a.xn, 0, H, w.wqkv.p16, 0, H, a.qkv, qkvw, 0));
-    k_rope(a.qkv, int(M), int(S), int(nh), int(d), float(L.model.rope_theta), 0, stream);
-    kcheck("rope");
+    {
+      // QKV projection with RoPE applied in the epilogue (d 64 / 128)
+      GemmDesc g = g2(M, qkvw, H, a.xn, 0, H, w.wqkv.p16, 0, H, a.qkv, qkvw, 0);
+      const bool fuse = cfg.fuse_rope && (d == 64 || d == 128);
+      if (fuse) {
+        g.rope = rope_tab_;
+        g.rope_d = int(d);
+        g.rope_S = int(S);
+      }
+      gemm(g);
+      if (!fuse) {
+        k_rope(a.qkv, int(M), int(S), int(nh), int(d), float(L.model.rope_theta), 0, stream);
+        kcheck("rope");
+      }
+    }
     attention_fwd(a);
     if (role.tp == 1) {
       GemmDesc g = g2(M, H, kr, a.attn, 0, kr, w.wo.p16, 1, H, a.x_mid, H, 1);

@@ -20,6 +20,7 @@ struct ExecConfig {
   bool profile_gemm = false;          // per-GEMM CUDA events (roofline evidence); eager
   bool graph_gemm_events = false;     // per-GEMM CUDA events inside the step graph
   bool fuse_swiglu = true;            // SwiGLU in the gate-up GEMM epilogue
+  bool fuse_rope = true;              // RoPE (forward) in the QKV GEMM epilogue
   // weight-gradient GEMMs over G token-concatenated micro-batches: -1 = auto
   // (all micro-batches that fit in memory), 0/1 = per micro-batch, G = force.
   // Off by default: +18-20 % wgrad throughput in isolation

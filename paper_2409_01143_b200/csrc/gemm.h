@@ -66,6 +66,11 @@ struct GemmDesc {
   // split / peers / batch.
   void* act = nullptr;
   long long ld_act = 0;
+  // RoPE epilogue (QKV projection, head-interleaved (h, {q,k,v}, d) columns):
+  // q and k of every head rotated (rotate-half) with (cos, sin) from
+  // rope[(row % rope_S) * rope_d / 2 + i]; d in {64, 128}; bf16 C only
+  const float2* rope = nullptr;
+  int rope_d = 0, rope_S = 0;
 };
 
 // workspace a GemmDesc needs for any split (bytes, counters)

@@ -50,6 +50,8 @@ struct EpiParams {
   int npeer;         // extra copies of every stored C tile (TP peers' buffers)
   int group_m;       // grouped tile raster (M-tiles per band), 0 = n fastest
   int act_mode;      // 1: SwiGLU epilogue, act = silu(g) * u to pm.m[0]
+  const float2* rope;  // RoPE epilogue: (cos, sin) table [rope_S][rope_d / 2], or null
+  int rope_d, rope_S;
   int mc;            // CTA pairs per cluster along N sharing the A tile (TMA multicast)
   int n_tiles_c;     // cluster tiles along N = ceil(n_tiles / mc)
 };
@@ -462,6 +464,57 @@ __global__ void __launch_bounds__(kThreads, 1)
             sb ^= 1;
           }
         }
+      } else if (row0 < p.M && p.rope) {
+        // RoPE epilogue (QKV projection): head-interleaved (h, {q, k, v}, d)
+        // columns; q and k blocks are rotated (rotate-half, pairs j / j + d/2)
+        // from the bf16-rounded values exactly as rope_kernel does, v passes.
+        // Position = row % S; angles from the precomputed (cos, sin) table.
+        const int dh = p.rope_d, half = dh / 2;
+        const float2* trow = p.rope + (long long)((row0 + lane) % p.rope_S) * half;
+#pragma unroll 1
+        for (int blk = 0; blk < BN; blk += dh) {
+          if (n0 + blk >= p.N) break;
+          const bool rot = ((n0 + blk) / dh) % 3 != 2;
+#pragma unroll 1
+          for (int c = 0; c < half; c += 32) {
+            uint32_t ra[32], rb[32];
+            const uint32_t tcol = tbase + (uint32_t(ew * 32) << 16) + uint32_t(acc * BN + blk + c);
+            tmem_ld_32x32b_x32(tcol, ra);
+            tmem_ld_32x32b_x32(tcol + half, rb);
+            tmem_ld_wait();
+            float xa[32], xb[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              xa[i] = __bfloat162float(__float2bfloat16(__uint_as_float(ra[i]) * p.alpha));
+              xb[i] = __bfloat162float(__float2bfloat16(__uint_as_float(rb[i]) * p.alpha));
+            }
+            if (rot) {
+#pragma unroll
+              for (int i = 0; i < 32; i += 2) {
+                const float4 t = __ldg(reinterpret_cast<const float4*>(trow + c + i));
+                const float cs0 = t.x, sn0 = t.y, cs1 = t.z, sn1 = t.w;
+                const float x0 = xa[i], y0 = xb[i], x1 = xa[i + 1], y1 = xb[i + 1];
+                xa[i] = x0 * cs0 - y0 * sn0;
+                xb[i] = y0 * cs0 + x0 * sn0;
+                xa[i + 1] = x1 * cs1 - y1 * sn1;
+                xb[i + 1] = y1 * cs1 + x1 * sn1;
+              }
+            }
+            if (lane == 0) bulk_wait_read<0>();
+            __syncwarp();
+            uint8_t* b0 = ebuf;
+            uint8_t* b1 = ebuf + C::EPI_CHUNK;
+            stage_chunk(b0, xa, false, lane);
+            stage_chunk(b1, xb, false, lane);
+            fence_async_shared();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_4d(&tmC, b0, n0 + blk + c, row0, z1, z2);
+              tma_store_4d(&tmC, b1, n0 + blk + half + c, row0, z1, z2);
+              bulk_commit();
+            }
+          }
+        }
       } else if (row0 < p.M) {
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
@@ -871,6 +924,12 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream) {
   PeerMaps pm;
   p.npeer = d.npeer;
   p.act_mode = d.act ? 1 : 0;
+  p.rope = d.rope;
+  p.rope_d = d.rope_d;
+  p.rope_S = d.rope_S;
+  if (d.rope && (d.act || d.npeer || d.beta || d.c_fp32 || d.R || d.nb1 * d.nb2 != 1 ||
+                 (d.rope_d != 64 && d.rope_d != 128) || d.N % (3 * d.rope_d) || d.rope_S <= 0))
+    return cudaErrorInvalidValue;
   if (d.act && (d.npeer || d.beta || d.c_fp32 || d.R || d.N % 128 || d.nb1 * d.nb2 != 1))
     return cudaErrorInvalidValue;
   if (d.npeer < 0 || d.npeer > kMaxGemmPeers) return cudaErrorInvalidValue;
@@ -891,7 +950,7 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream) {
   p.ws = d.ws;
   p.ws_cnt = d.ws_cnt;
   CUtensorMap mw = mc;
-  if (d.causal == kCausalNone && d.split != 0 && d.npeer == 0 && !d.act && p.mc == 1 &&
+  if (d.causal == kCausalNone && d.split != 0 && d.npeer == 0 && !d.act && !d.rope && p.mc == 1 &&
       p.num_tiles > 0) {
     const int kblocks = (d.K + BK - 1) / BK;
     const bool direct = d.beta && !d.R;

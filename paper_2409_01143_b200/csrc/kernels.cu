@@ -432,6 +432,20 @@ __global__ void __launch_bounds__(1024) colsum_add_kernel(const float* __restric
 // sin/cos pairs are computed once and applied to q and k of every head in
 // the group; 16-byte loads of both halves, all loads of the group in flight
 constexpr int kRopeHeads = 4;
+// (cos, sin) of position p and rotation pair i, the same expressions as below
+__global__ void rope_table_kernel(float2* tab, int S, int d, float theta) {
+  const int half = d / 2;
+  const float l2t = log2f(theta);
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < S * half;
+       idx += gridDim.x * blockDim.x) {
+    const int i = idx % half;
+    const float pos = float(idx / half);
+    const float inv_freq = exp2f(-2.0f * float(i) / float(d) * l2t);
+    float sn, cs;
+    sincosf(pos * inv_freq, &sn, &cs);
+    tab[idx] = make_float2(cs, sn);
+  }
+}
 __global__ void rope_kernel(bf16* qkv, int M, int S, int nh, int d, float theta, int inverse) {
   const int half = d / 2;
   const int g8 = half / 8;
@@ -892,6 +906,10 @@ void k_rmsnorm_bwd(const bf16* dyb, const float* dyf, const float* x, const floa
 #undef HX_NORM_BWD_NC
 #undef HX_NORM_BWD
   colsum_add_kernel<<<(H + 31) / 32, 1024, 0, s>>>(dg_part, grid, H, dg);
+}
+void k_rope_table(float2* tab, int S, int d, float theta, cudaStream_t s) {
+  const int n = S * (d / 2);
+  if (n > 0) rope_table_kernel<<<std::min(1184, (n + 255) / 256), 256, 0, s>>>(tab, S, d, theta);
 }
 void k_rope(bf16* qkv, int M, int S, int nh, int d, float theta, int inverse, cudaStream_t s) {
   long long n = (long long)M * ((nh + kRopeHeads - 1) / kRopeHeads) * (d / 16);

@@ -106,6 +106,8 @@ void k_peer_copy(void* dst, const void* src, size_t bytes, int sms, cudaStream_t
 // in-place rotary embedding of q and k inside the fused [M, nh*3*d] buffer
 // (rotate-half convention); inverse=1 applies the transpose (backward).
 void k_rope(bf16* qkv, int M, int S, int nh, int d, float theta, int inverse, cudaStream_t s);
+// (cos, sin) table [S][d/2] of the same angles (for the GEMM's RoPE epilogue)
+void k_rope_table(float2* tab, int S, int d, float theta, cudaStream_t s);
 
 // causal softmax over fp32 scores [nb][L][L] (already scaled); P bf16 with
 // zeros for j > i up to the end of the row's 128-wide tile.

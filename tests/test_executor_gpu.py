@@ -272,3 +272,21 @@ def test_large_layer_shapes_sharding_invariance(tmp_path, shape):
                 row0 = int(r[t + "|row0"])
                 ref = one[0][key][row0:row0 + r[key].shape[0]]
                 assert rel(r[key], ref) < 3e-2, (key, rel(r[key], ref))
+
+
+@pytest.mark.parametrize("name", ["tiny_1", "tiny_tp31", "llama13b_2l_1gpu"])
+def test_rope_epilogue_matches_kernel(tmp_path, name):
+    """RoPE applied in the QKV GEMM epilogue (table of the same angles, from the
+    bf16-rounded q / k) == the standalone rope kernel (d = 64 and 128)."""
+    only = r"^(layers\.0\.wqkv|lm_head)$"
+    fused = run_plan(name, tmp_path / "fused", steps=2, xcfg={"fuse_rope": True}, read=only)
+    plain = run_plan(name, tmp_path / "plain", steps=2, xcfg={"fuse_rope": False}, read=only)
+    if name.startswith("tiny"):
+        check_against_oracle_subset = oracle_for(name)  # noqa: F841 (oracle loss below)
+        assert abs(float(fused[0]["losses"][0]) - check_against_oracle_subset[0]) <= \
+            RTOL * abs(check_against_oracle_subset[0])
+    for a, b in zip(fused, plain):
+        assert np.allclose(a["losses"], b["losses"], rtol=1e-5, atol=0), (a["losses"], b["losses"])
+        for key in a:
+            if key.endswith("|grad"):
+                assert rel(a[key], b[key]) < 1e-3, (key, rel(a[key], b[key]))
