@@ -1011,6 +1011,82 @@ __global__ void attn_dq_cast_kernel(const float* __restrict__ dq, __nv_bfloat16*
   }
 }
 
+// dq cast fused with the RoPE backward (inverse rotation) of dq and dk: thread
+// per (row, head, 8 rotation pairs).  dq is rounded to bf16 first and dk read
+// as bf16, exactly the values the standalone rope kernel would rotate; (cos,
+// sin) from the forward epilogue's table tab[pos][D/2], sin negated.
+__device__ __forceinline__ void bf16x8_to_f32(uint4 w, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    f[2 * k] = __low2float(h[k]);
+    f[2 * k + 1] = __high2float(h[k]);
+  }
+}
+__device__ __forceinline__ uint4 f32x8_to_bf16(const float* f) {
+  uint4 w;
+  w.x = pack_bf16x2(f[0], f[1]);
+  w.y = pack_bf16x2(f[2], f[3]);
+  w.z = pack_bf16x2(f[4], f[5]);
+  w.w = pack_bf16x2(f[6], f[7]);
+  return w;
+}
+template <int D>
+__global__ void attn_dq_cast_rope_kernel(const float* __restrict__ dq, __nv_bfloat16* __restrict__ dqkv,
+                                         const float2* __restrict__ tab, long long M, int S, int nh) {
+  constexpr int half = D / 2, g8 = half / 8;
+  const long long n = M * nh * g8;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int c = int(idx % g8);
+    const long long t = idx / g8;
+    const int h = int(t % nh);
+    const long long row = t / nh;
+    const float4* tp = reinterpret_cast<const float4*>(tab + (row % S) * half + c * 8);
+    float cs[8], sn[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 v = __ldg(tp + k);
+      cs[2 * k] = v.x;
+      sn[2 * k] = -v.y;
+      cs[2 * k + 1] = v.z;
+      sn[2 * k + 1] = -v.w;
+    }
+    const float* src = dq + row * nh * D + h * D + c * 8;
+    __nv_bfloat16* qb = dqkv + row * 3LL * nh * D + (long long)h * 3 * D + c * 8;
+    __nv_bfloat16* kb = qb + D;
+    float qa[8], qh[8], ka[8], kh[8];
+    {
+      const float4 a0 = reinterpret_cast<const float4*>(src)[0], a1 = reinterpret_cast<const float4*>(src)[1];
+      const float4 b0 = reinterpret_cast<const float4*>(src + half)[0];
+      const float4 b1 = reinterpret_cast<const float4*>(src + half)[1];
+      const float fa[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float fb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        qa[k] = __bfloat162float(__float2bfloat16(fa[k]));
+        qh[k] = __bfloat162float(__float2bfloat16(fb[k]));
+      }
+    }
+    bf16x8_to_f32(*reinterpret_cast<const uint4*>(kb), ka);
+    bf16x8_to_f32(*reinterpret_cast<const uint4*>(kb + half), kh);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float x = qa[k], y = qh[k];
+      qa[k] = x * cs[k] - y * sn[k];
+      qh[k] = y * cs[k] + x * sn[k];
+      x = ka[k];
+      y = kh[k];
+      ka[k] = x * cs[k] - y * sn[k];
+      kh[k] = y * cs[k] + x * sn[k];
+    }
+    *reinterpret_cast<uint4*>(qb) = f32x8_to_bf16(qa);
+    *reinterpret_cast<uint4*>(qb + half) = f32x8_to_bf16(qh);
+    *reinterpret_cast<uint4*>(kb) = f32x8_to_bf16(ka);
+    *reinterpret_cast<uint4*>(kb + half) = f32x8_to_bf16(kh);
+  }
+}
+
 // ------------------------------------------------------------------ host
 int g_fwd_variant = 2;  // 2 = two query tiles per CTA (ping-pong), 1 = one tile
 PFN_cuTensorMapEncodeTiled_v12000 g_enc = nullptr;
@@ -1127,7 +1203,11 @@ cudaError_t launch_bwd(const AttnBwdDesc& a, cudaStream_t s) {
   p.scale_log2 = a.scale * 1.4426950408889634f;
   const int grid = (a.S / T) * a.nh * a.mb;
   attn_bwd_kernel<D><<<grid, kBwdThreads, C::SMEM, s>>>(q, k, v, dO, dq, p);
-  attn_dq_cast_kernel<D><<<ew_blocks(M * a.nh * (D / 8)), 256, 0, s>>>(a.dq_acc, a.dqkv, M, a.nh);
+  if (a.rope)
+    attn_dq_cast_rope_kernel<D><<<ew_blocks(M * a.nh * (D / 16)), 256, 0, s>>>(a.dq_acc, a.dqkv, a.rope,
+                                                                              M, a.S, a.nh);
+  else
+    attn_dq_cast_kernel<D><<<ew_blocks(M * a.nh * (D / 8)), 256, 0, s>>>(a.dq_acc, a.dqkv, M, a.nh);
   return cudaGetLastError();
 }
 

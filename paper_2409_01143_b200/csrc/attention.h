@@ -32,6 +32,9 @@ struct AttnBwdDesc {
   __nv_bfloat16* dqkv = nullptr;        // [M, nh*3*d]: dq, dk, dv written in place
   int S = 0, nh = 0, d = 0, mb = 0;
   float scale = 1.f;
+  // optional RoPE backward fused into the dq cast: (cos, sin) table [S][d/2]
+  // of the forward rotation; dq and dk of dqkv come out un-rotated
+  const float2* rope = nullptr;
 };
 
 // backward: dq, dk, dv of the forward above

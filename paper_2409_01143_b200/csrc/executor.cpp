@@ -1252,9 +1252,11 @@ class Executor {
     gemm(g2(M, kr, H, dxmb, 0, H, w.wo.p16, 0, H, dattn, kr, 0));
     if (do_wgrad)
       wgemm(kr, grouped ? st->attn : a.attn, kr, grouped ? st->dxmb : dxmb, H, w.wo.g32);
-    attention_bwd(a);
-    k_rope(dqkv, int(M), int(S), int(nh), int(d), float(L.model.rope_theta), 1, stream);
-    kcheck("rope");
+    // RoPE backward: fused into the fused attention's dq cast (d 64 / 128)
+    if (!attention_bwd(a, cfg.fuse_rope && (d == 64 || d == 128))) {
+      k_rope(dqkv, int(M), int(S), int(nh), int(d), float(L.model.rope_theta), 1, stream);
+      kcheck("rope");
+    }
     if (tp_peer_)
       dyr = tp_partial_gemm(g2(M, H, qkvw, dqkv, 0, qkvw, w.wqkv.p16, 1, H, nullptr, H, 0));
     else
@@ -1272,7 +1274,8 @@ class Executor {
     dqkv = dqkv_saved;
   }
 
-  void attention_bwd(LayerActs& a) {
+  // returns true when the RoPE backward was applied (fused path with rope)
+  bool attention_bwd(LayerActs& a, bool rope) {
     if (cfg.attention == "fused") {
       AttnBwdDesc ad;
       ad.qkv = a.qkv;
@@ -1287,11 +1290,12 @@ class Executor {
       ad.d = int(d);
       ad.mb = int(mb);
       ad.scale = 1.f / std::sqrt(float(d));
+      if (rope) ad.rope = rope_tab_;
       cudaError_t e = hexexec::attention_bwd(ad, stream);
       if (e != cudaSuccess) throw CudaError(std::string("attention_bwd: ") + cudaGetErrorString(e));
       launches_step += 2;  // delta + dq cast kernels (+ the main kernel below)
       kcheck("attn_bwd");
-      return;
+      return ad.rope != nullptr;
     }
     gemm_kind_ = 1;
     const int64_t SS2 = S * S;
@@ -1343,6 +1347,7 @@ class Executor {
     v.causal = kCausalKUpper;
     gemm(v);
     gemm_kind_ = 0;
+    return false;
   }
 
   // backward of one micro-batch; dx_top (fp32) is the grad of the stage output

@@ -277,7 +277,8 @@ def test_large_layer_shapes_sharding_invariance(tmp_path, shape):
 @pytest.mark.parametrize("name", ["tiny_1", "tiny_tp31", "llama13b_2l_1gpu"])
 def test_rope_epilogue_matches_kernel(tmp_path, name):
     """RoPE applied in the QKV GEMM epilogue (table of the same angles, from the
-    bf16-rounded q / k) == the standalone rope kernel (d = 64 and 128)."""
+    bf16-rounded q / k) and its inverse fused into the attention backward's dq
+    cast == the standalone rope kernel in both directions (d = 64 and 128)."""
     only = r"^(layers\.0\.wqkv|lm_head)$"
     fused = run_plan(name, tmp_path / "fused", steps=2, xcfg={"fuse_rope": True}, read=only)
     plain = run_plan(name, tmp_path / "plain", steps=2, xcfg={"fuse_rope": False}, read=only)
