@@ -1072,13 +1072,14 @@ __global__ void attn_dq_cast_rope_kernel(const float* __restrict__ dq, __nv_bflo
     bf16x8_to_f32(*reinterpret_cast<const uint4*>(kb + half), kh);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
+      // explicit rounding, as rope_kernel
       float x = qa[k], y = qh[k];
-      qa[k] = x * cs[k] - y * sn[k];
-      qh[k] = y * cs[k] + x * sn[k];
+      qa[k] = __fsub_rn(__fmul_rn(x, cs[k]), __fmul_rn(y, sn[k]));
+      qh[k] = __fadd_rn(__fmul_rn(y, cs[k]), __fmul_rn(x, sn[k]));
       x = ka[k];
       y = kh[k];
-      ka[k] = x * cs[k] - y * sn[k];
-      kh[k] = y * cs[k] + x * sn[k];
+      ka[k] = __fsub_rn(__fmul_rn(x, cs[k]), __fmul_rn(y, sn[k]));
+      kh[k] = __fadd_rn(__fmul_rn(y, cs[k]), __fmul_rn(x, sn[k]));
     }
     *reinterpret_cast<uint4*>(qb) = f32x8_to_bf16(qa);
     *reinterpret_cast<uint4*>(qb + half) = f32x8_to_bf16(qh);

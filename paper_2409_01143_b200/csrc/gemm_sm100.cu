@@ -494,10 +494,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const float4 t = __ldg(reinterpret_cast<const float4*>(trow + c + i));
                 const float cs0 = t.x, sn0 = t.y, cs1 = t.z, sn1 = t.w;
                 const float x0 = xa[i], y0 = xb[i], x1 = xa[i + 1], y1 = xb[i + 1];
-                xa[i] = x0 * cs0 - y0 * sn0;
-                xb[i] = y0 * cs0 + x0 * sn0;
-                xa[i + 1] = x1 * cs1 - y1 * sn1;
-                xb[i + 1] = y1 * cs1 + x1 * sn1;
+                // explicit rounding, as rope_kernel
+                xa[i] = __fsub_rn(__fmul_rn(x0, cs0), __fmul_rn(y0, sn0));
+                xb[i] = __fadd_rn(__fmul_rn(y0, cs0), __fmul_rn(x0, sn0));
+                xa[i + 1] = __fsub_rn(__fmul_rn(x1, cs1), __fmul_rn(y1, sn1));
+                xb[i + 1] = __fadd_rn(__fmul_rn(y1, cs1), __fmul_rn(x1, sn1));
               }
             }
             if (lane == 0) bulk_wait_read<0>();

@@ -478,9 +478,11 @@ __global__ void rope_kernel(bf16* qkv, int M, int S, int nh, int d, float theta,
       unpack8(*reinterpret_cast<const uint4*>(base + half), b);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
+        // explicit rounding (no FMA contraction): the same values as the
+        // fused epilogue / dq-cast rotations and the numpy oracle
         const float x = a[k], y = b[k];
-        a[k] = x * cs[k] - y * sn[k];
-        b[k] = y * cs[k] + x * sn[k];
+        a[k] = __fsub_rn(__fmul_rn(x, cs[k]), __fmul_rn(y, sn[k]));
+        b[k] = __fadd_rn(__fmul_rn(y, cs[k]), __fmul_rn(x, sn[k]));
       }
       *reinterpret_cast<uint4*>(base) = pack8(a);
       *reinterpret_cast<uint4*>(base + half) = pack8(b);
