@@ -21,6 +21,9 @@ over pipelines (the DP allreduce); AdamW updates the global weights.
 """
 from __future__ import annotations
 
+import os
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 
 from . import bookkeeping as bk
@@ -31,18 +34,71 @@ TENSOR_IDS = {"embed": 0, "attn_norm": 1, "wqkv": 2, "wo": 3, "mlp_norm": 4, "wg
               "wdown": 6, "final_norm": 7, "lm_head": 8}
 
 
+def _pool() -> ThreadPoolExecutor:
+    """Host threads for the per-head attention loops and the weight init (numpy
+    releases the GIL inside ufuncs / BLAS, so threads scale on the host cores;
+    the arithmetic of every element is unchanged)."""
+    global _POOL
+    if _POOL is None:
+        n = int(os.environ.get("HEXEXEC_THREADS", "0")) or (len(os.sched_getaffinity(0))
+                                                          if hasattr(os, "sched_getaffinity")
+                                                          else os.cpu_count() or 1)
+        _POOL = ThreadPoolExecutor(max_workers=max(1, n))
+    return _POOL
+
+
+_POOL = None
+
+
+def _blas1():
+    """One BLAS thread per worker while the per-head pool runs (process-global)."""
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(1, "blas")
+    except ImportError:  # pragma: no cover
+        import contextlib
+        return contextlib.nullcontext()
+
+
 def init_weights(m: dict, seed: int) -> dict:
     """Global fp32 weights; tensor seed = mix_seed(seed, layer + 1, tensor_id),
     element seed = splitmix64(tensor_seed + global row-major index)."""
     W = {}
+    chunk = 1 << 22
     for t in bk.catalogue(m):
         base = t["name"].split(".")[-1]
         if t["kind"] in ("norm", "final_norm"):
             W[t["name"]] = np.ones((t["rows"], t["cols"]), F32)
         else:
             s = rng.mix_seed(seed, t["layer"] + 1, TENSOR_IDS[base])
-            W[t["name"]] = rng.init_normal(s, 0, t["rows"] * t["cols"]).reshape(t["rows"], t["cols"])
+            n = t["rows"] * t["cols"]
+            out = np.empty(n, F32)
+
+            def fill(o, s=s, n=n, out=out):
+                out[o:min(n, o + chunk)] = rng.init_normal(s, o, min(chunk, n - o))
+            list(_pool().map(fill, range(0, n, chunk)))
+            W[t["name"]] = out.reshape(t["rows"], t["cols"])
     return W
+
+
+def attn_fwd_head(q, k, v, d):
+    """One (sample, head): causal softmax(q k^T / sqrt(d)) v, fp32.  Returns (P, o)."""
+    S = q.shape[0]
+    s = (q @ k.T) / F32(np.sqrt(d))
+    s = np.where(np.triu(np.ones((S, S), bool), 1), -np.inf, s)
+    s = s - s.max(-1, keepdims=True)
+    e = np.exp(s)
+    P = (e / e.sum(-1, keepdims=True)).astype(F32)
+    return P, P @ v
+
+
+def attn_bwd_head(P, q, k, v, dO, d):
+    """Backward of attn_fwd_head: (dq, dk, dv) before the RoPE inverse."""
+    dV = P.T @ dO
+    dP = dO @ v.T
+    Dv = (P * dP).sum(-1, keepdims=True)
+    dS = P * (dP - Dv) / F32(np.sqrt(d))
+    return dS @ k, dS.T @ q, dV
 
 
 # ---------------------------------------------------------------- primitives
@@ -128,13 +184,14 @@ class Step:
             q = rope(t[:, :, 0], cos, sin)
             k = rope(t[:, :, 1], cos, sin)
             v = t[:, :, 2].astype(F32)
-            s = (q @ k.transpose(0, 1, 3, 2)) / F32(np.sqrt(d))
-            mask = np.triu(np.ones((S, S), bool), 1)
-            s = np.where(mask, -np.inf, s)
-            s = s - s.max(-1, keepdims=True)
-            e = np.exp(s)
-            P = (e / e.sum(-1, keepdims=True)).astype(F32)
-            o = P @ v                                                    # [mb, nr, S, d]
+            P = np.empty((mb, nr, S, S), F32)
+            o = np.empty((mb, nr, S, d), F32)                            # [mb, nr, S, d]
+
+            def head(i):
+                b, h = divmod(i, nr)
+                P[b, h], o[b, h] = attn_fwd_head(q[b, h], k[b, h], v[b, h], d)
+            with _blas1():
+                list(_pool().map(head, range(mb * nr)))
             attn = o.transpose(0, 2, 1, 3).reshape(mb * S, nr * d)
             y += attn @ W[p + "wo"][d * h0:d * h1]
             c["parts"].append(dict(q=q, k=k, v=v, P=P, attn=attn))
@@ -179,12 +236,19 @@ class Step:
             G[p + "wo"][d * h0:d * h1] += ap["attn"].T @ dx_mid
             dattn = dx_mid @ W[p + "wo"][d * h0:d * h1].T
             dO = dattn.reshape(mb, S, nr, d).transpose(0, 2, 1, 3)
-            dV = ap["P"].transpose(0, 1, 3, 2) @ dO
-            dP = dO @ ap["v"].transpose(0, 1, 3, 2)
-            Dv = (ap["P"] * dP).sum(-1, keepdims=True)
-            dS = ap["P"] * (dP - Dv) / F32(np.sqrt(d))
-            dq = rope(dS @ ap["k"], cos, sin, inverse=True)
-            dk = rope(dS.transpose(0, 1, 3, 2) @ ap["q"], cos, sin, inverse=True)
+            dq = np.empty((mb, nr, S, d), F32)
+            dk = np.empty((mb, nr, S, d), F32)
+            dV = np.empty((mb, nr, S, d), F32)
+
+            def head(i, ap=ap, dO=dO, dq=dq, dk=dk, dV=dV):
+                b, h = divmod(i, nr)
+                dq[b, h], dk[b, h], dV[b, h] = attn_bwd_head(
+                    ap["P"][b, h], ap["q"][b, h], ap["k"][b, h], ap["v"][b, h],
+                    np.ascontiguousarray(dO[b, h]), d)
+            with _blas1():
+                list(_pool().map(head, range(mb * nr)))
+            dq = rope(dq, cos, sin, inverse=True)
+            dk = rope(dk, cos, sin, inverse=True)
             dqkv = np.stack([dq, dk, dV], 2).transpose(0, 3, 1, 2, 4).reshape(mb * S, nr * 3 * d)
             G[p + "wqkv"][3 * d * h0:3 * d * h1] += dqkv.T @ c["xn"]
             dxn += dqkv @ W[p + "wqkv"][3 * d * h0:3 * d * h1]

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 
 #include "attention.h"
@@ -407,17 +408,29 @@ hexexec_status hexexec_k_rmsnorm_bwd(const void* dyb, const float* dyf, const fl
                                      const float* rstd, const float* g, const float* dres,
                                      float* dx, void* dxb, float* dg, int M, int H,
                                      void* stream) {
-  // partial-dg scratch kept across calls (grown on demand; kernel entry only)
-  static float* part = nullptr;
-  static size_t cap = 0;
+  // partial-dg scratch kept across calls, one per device and host thread
+  // (grown on demand; kernel test entry only -- the executor passes its own).
+  // Calls from one thread on one device are stream-ordered by the caller.
+  struct Scratch {
+    float* part = nullptr;
+    size_t cap = 0;
+  };
+  static thread_local std::map<int, Scratch> scratch;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return HEXEXEC_ERR_CUDA;
+  Scratch& sc = scratch[dev];
   const size_t need = size_t(hexexec::kRmsBwdCtas) * size_t(H > 0 ? H : 1) * sizeof(float);
-  if (need > cap) {
-    if (part) cudaFree(part);
-    part = nullptr;
-    cap = 0;
-    if (cudaMalloc(&part, need) != cudaSuccess) return HEXEXEC_ERR_CUDA;
-    cap = need;
+  if (need > sc.cap) {
+    if (sc.part) {
+      cudaStreamSynchronize(as_stream(stream));  // the old scratch may still be read
+      cudaFree(sc.part);
+    }
+    sc.part = nullptr;
+    sc.cap = 0;
+    if (cudaMalloc(&sc.part, need) != cudaSuccess) return HEXEXEC_ERR_CUDA;
+    sc.cap = need;
   }
+  float* part = sc.part;
   hexexec::k_rmsnorm_bwd(static_cast<const hexexec::bf16*>(dyb), dyf, x, rstd, g, dres, dx,
                          static_cast<hexexec::bf16*>(dxb), dg, M, H, part, as_stream(stream));
   return cuda_status(cudaGetLastError());

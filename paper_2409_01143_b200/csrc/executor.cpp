@@ -256,7 +256,9 @@ class Executor {
   cudaEvent_t* ev = ev_eager_;  // phase events of the mode that ran last
   cudaEvent_t tmr_[2] = {};
   float phase_ms[5] = {0, 0, 0, 0, 0};
-  int64_t launches_step = 0, launches_total = 0;
+  // kernel launches of ours per step; copies_step counts the step's memset /
+  // memcpy nodes separately (not kernels)
+  int64_t launches_step = 0, launches_total = 0, copies_step = 0;
   int64_t nccl_calls_step = 0;
   float last_loss = 0.f;
 
@@ -1006,6 +1008,7 @@ class Executor {
       if (cfg.tp_pull == "ce") {
         HX_CUDA(cudaMemcpyAsync(xslot(tpp_.me, b, tp_crit_), xslot(tp_crit_, b, tp_crit_),
                                 tp_slot_elems() * 2, cudaMemcpyDeviceToDevice, stream));
+        ++copies_step;
       } else {
         k_peer_copy(xslot(tpp_.me, b, tp_crit_), xslot(tp_crit_, b, tp_crit_),
                     tp_slot_elems() * 2, sm_applied, stream);
@@ -1180,6 +1183,7 @@ class Executor {
       tp_allreduce_f32(st2, st2, 2 * M, ncclSum);
     } else {
       HX_CUDA(cudaMemcpyAsync(gmax, lmax, size_t(M) * 4, cudaMemcpyDeviceToDevice, stream));
+      ++copies_step;
     }
     const float inv_count = 1.f / float(role.batch * S);
     k_ce_finish(logits, int(Vr), int(v0), tk, int(M), int(S), gmax, st2, inv_count, sl.dlogits,
@@ -1294,6 +1298,7 @@ class Executor {
       cudaError_t e = hexexec::attention_bwd(ad, stream);
       if (e != cudaSuccess) throw CudaError(std::string("attention_bwd: ") + cudaGetErrorString(e));
       launches_step += 2;  // delta + dq cast kernels (+ the main kernel below)
+      ++copies_step;       // the dq accumulator memset
       kcheck("attn_bwd");
       return ad.rope != nullptr;
     }
@@ -1391,6 +1396,7 @@ class Executor {
       group_ready(kGroupHead);
     } else {
       HX_CUDA(cudaMemcpyAsync(cur, dx_top, size_t(M * H) * 4, cudaMemcpyDeviceToDevice, stream));
+      ++copies_step;
       k_cast_bf16(cur, curb, M * H, stream);
       kcheck("cast_bf16");
     }
@@ -1427,10 +1433,19 @@ class Executor {
     HX_NCCL(ncclRecv(buf, size_t(M * H), ncclFloat32, peer, world_comm, stream));
     ++nccl_calls_step;
   }
-  // leader protocol, after the receive has completed (outside the P2P group)
+  // leader protocol, after the receive has completed (outside the P2P group).
+  // The root is the leader's rank in the TP communicator: that communicator
+  // is keyed by position in the sorted rank set (setup_comms), which differs
+  // from tp order when a stage lists its devices out of rank order or the
+  // cluster's `rank` extension permutes them.
+  int leader_comm_rank() const {
+    const auto& set = L.comm_sets[size_t(L.tp_comm[size_t(rank)])];
+    return int(std::find(set.begin(), set.end(), role.tp_group[0]) - set.begin());
+  }
   void bcast_in_stage(int peer, float* buf) {
     if (peer < 0 || !pp_leader() || role.tp <= 1) return;
-    HX_NCCL(ncclBroadcast(buf, buf, size_t(M * H), ncclFloat32, 0, tp_comm(), stream));
+    HX_NCCL(ncclBroadcast(buf, buf, size_t(M * H), ncclFloat32, leader_comm_rank(), tp_comm(),
+                          stream));
     ++nccl_calls_step;
   }
   void send_fwd(Slot& sl) { send_to(role.fwd_send_to, sl.x[size_t(nl)]); }
@@ -1713,6 +1728,7 @@ class Executor {
 
   void enqueue_body() {
     launches_step = 0;
+    copies_step = 0;
     xop_ = 0;
     nccl_calls_step = 0;
     cudaEventRecordWithFlags(ev[0], stream, capturing_ ? cudaEventRecordExternal : 0);
@@ -1724,11 +1740,14 @@ class Executor {
       kcheck("gen_tokens");
     }
     HX_CUDA(cudaMemsetAsync(loss_acc, 0, 4, stream));
+    ++copies_step;
     // zero the atomically-accumulated grads (norm gains, embedding)
     for (const auto& rt : role.tensors) {
       const TensorSpec& ts = L.tensors[size_t(rt.spec)];
-      if (ts.id == kAttnNorm || ts.id == kMlpNorm || ts.id == kFinalNorm || ts.id == kEmbed)
+      if (ts.id == kAttnNorm || ts.id == kMlpNorm || ts.id == kFinalNorm || ts.id == kEmbed) {
         HX_CUDA(cudaMemsetAsync(G32 + rt.offset, 0, size_t(rt.rows * ts.cols) * 4, stream));
+        ++copies_step;
+      }
     }
     mark("prologue");
     cudaEventRecordWithFlags(ev[1], stream, capturing_ ? cudaEventRecordExternal : 0);
@@ -1818,6 +1837,7 @@ class Executor {
     j["steps"] = step_index;
     j["launches_last_step"] = launches_step;
     j["launches_total"] = launches_total;
+    j["copy_nodes_last_step"] = copies_step;
     j["nccl_calls_last_step"] = nccl_calls_step;
     j["ms"] = {{"prologue", phase_ms[0]}, {"pipeline", phase_ms[1]}, {"dp_sync", phase_ms[2]},
                {"optimizer", phase_ms[3]}, {"step", phase_ms[4]}};

@@ -478,8 +478,9 @@ __global__ void rope_kernel(bf16* qkv, int M, int S, int nh, int d, float theta,
       unpack8(*reinterpret_cast<const uint4*>(base + half), b);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        // explicit rounding (no FMA contraction): the same values as the
-        // fused epilogue / dq-cast rotations and the numpy oracle
+        // explicit rounding (no FMA contraction): bitwise the same values as
+        // the QKV-epilogue and dq-cast rotations (the oracle's float64 tables
+        // differ in the last bits; it is compared within tolerance)
         const float x = a[k], y = b[k];
         a[k] = __fsub_rn(__fmul_rn(x, cs[k]), __fmul_rn(y, sn[k]));
         b[k] = __fadd_rn(__fmul_rn(y, cs[k]), __fmul_rn(x, sn[k]));

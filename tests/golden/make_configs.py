@@ -91,6 +91,15 @@ MODELS = {
     "llama30b_2l_s256": {"num_layers": 2, "hidden_dim": 6656, "seq_len": 256,
                          "bytes_per_element": 2, "num_heads": 52, "ffn_dim": 17920,
                          "vocab_size": 1024},
+    # the benchmarked 7B shape (H 4096, 32 heads, F 11008, V 32000, S 2048) cut
+    # to 2 layers: GPU-vs-oracle parity of the headline workload's kernels
+    "llama7b_2l": {"num_layers": 2, "hidden_dim": 4096, "seq_len": 2048, "bytes_per_element": 2,
+                   "num_heads": 32, "ffn_dim": 11008, "vocab_size": 32000},
+    # 13B layer shapes, 4 layers: the 4-GPU analogues of cfg4 (3-stage PP with an
+    # uneven TP stage) and of a mixed TP + PP + DP plan, against the oracle
+    "llama13b_4l_s256": {"num_layers": 4, "hidden_dim": 5120, "seq_len": 256,
+                         "bytes_per_element": 2, "num_heads": 40, "ffn_dim": 13824,
+                         "vocab_size": 1024},
 }
 
 
@@ -129,6 +138,10 @@ HAND = {
         pipe(3, 1, [stage(["g1"], 0, 4)])], 4)),
     "tiny_pp3_4": ("b200_4_tiers", "tiny", plan([pipe(8, 2, [
         stage(["g0"], 0, 2), stage(["g2", "g3"], 2, 1, [1, 3]), stage(["g1"], 3, 1)])], 4)),
+    # same pipeline, middle stage listed out of rank order ([g3, g2], widths 3:1):
+    # its TP communicator's rank 0 (lowest world rank) is not the stage leader
+    "tiny_pp3_4_perm": ("b200_4_tiers", "tiny", plan([pipe(8, 2, [
+        stage(["g0"], 0, 2), stage(["g3", "g2"], 2, 1, [3, 1]), stage(["g1"], 3, 1)])], 4)),
     # N=1 workload: the cfg2 model on one B200
     "llama7b_4l_1gpu": ("b200_1", "llama7b_4l", plan([pipe(8, 1, [stage(["g0"], 0, 4)])], 4)),
     # cfg2: Llama-7B 4-layer block, TP=2 with 3:1 widths, rank 1 capped to 1/3 SMs
@@ -151,6 +164,20 @@ HAND = {
     "llama30b_2l_1gpu": ("b200_1", "llama30b_2l_s256", plan([pipe(2, 1, [stage(["g0"], 0, 2)])], 2)),
     "llama30b_2l_tp31": ("b200_2_capped", "llama30b_2l_s256",
                          plan([pipe(2, 1, [stage(["g0", "g1"], 0, 2, [3, 1])])], 2)),
+    # oracle parity at the benchmarked 7B shape: one B200, and TP 3:1 on the
+    # capped pair (shards 24/8 heads, 8256/2752 FFN columns, 24000/8000 vocab rows)
+    "llama7b_2l_1gpu": ("b200_1", "llama7b_2l", plan([pipe(2, 1, [stage(["g0"], 0, 2)])], 2)),
+    "llama7b_2l_tp31": ("b200_2_capped", "llama7b_2l",
+                        plan([pipe(2, 1, [stage(["g0", "g1"], 0, 2, [3, 1])])], 2)),
+    # cfg4 analogue on 4 GPUs at 13B layer shapes: 3 stages with an uneven layer
+    # split 2/1/1 and an uneven TP stage (3:1 over a full and a half-capped B200)
+    "llama13b_4l_pp3": ("b200_4_tiers", "llama13b_4l_s256", plan([pipe(4, 1, [
+        stage(["g0"], 0, 2), stage(["g1", "g2"], 2, 1, [3, 1]), stage(["g3"], 3, 1)])], 4)),
+    # mixed TP + PP + DP at 13B layer shapes: pipeline 0 = TP 2:1 stage (3 layers)
+    # + 1-layer stage, 3 samples; pipeline 1 = one B200, 2 samples
+    "llama13b_4l_mixed": ("b200_4_tiers", "llama13b_4l_s256", plan([
+        pipe(3, 1, [stage(["g0", "g2"], 0, 3, [2, 1]), stage(["g3"], 3, 1)]),
+        pipe(2, 1, [stage(["g1"], 0, 4)])], 4)),
     # the pipelines of the calibrated 8-GPU plan (llama7b_8_cal) run alone:
     # P0 / P1 = PP 16/16 on two full B200s (21 samples); P2 = TP 2 on the half
     # tier (20 layers) + TP 2 on the third tier (12 layers), 22 samples

@@ -7,11 +7,6 @@ reduced gradients and updated weights, relative for the loss.
 Multi-rank plans need that many GPUs; they are skipped otherwise.
 """
 import json
-import os
-import socket
-import subprocess
-import sys
-import time
 
 import numpy as np
 import pytest
@@ -19,116 +14,7 @@ import pytest
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-CFG = os.path.join(ROOT, "configs")
-INDEX = json.load(open(os.path.join(CFG, "index.json")))
-RTOL = 2e-2
-
-
-def ngpu():
-    return torch.cuda.device_count() if torch.cuda.is_available() else 0
-
-
-def free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
-
-
-def run_plan(name, tmp_path, steps=1, xcfg=None, host_tokens=True, timeout=600, read=None):
-    for attempt in range(3):  # a rendezvous port taken between probe and bind: retry
-        try:
-            return _run_plan(name, tmp_path, steps, xcfg, host_tokens, timeout, read)
-        except PortInUse:
-            continue
-    raise RuntimeError("no free rendezvous port")
-
-
-class PortInUse(Exception):
-    pass
-
-
-def _run_plan(name, tmp_path, steps, xcfg, host_tokens, timeout, read=None):
-    e = INDEX[name]
-    world = len(json.load(open(os.path.join(CFG, "clusters", e["cluster"] + ".json")))["devices"])
-    if ngpu() < world:
-        pytest.skip(f"{name} needs {world} GPUs")
-    os.makedirs(tmp_path, exist_ok=True)
-    port = free_port()
-    procs, logs = [], []
-    for r in range(world):
-        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), LOCAL_RANK=str(r),
-                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-        if read:
-            env["HEXEXEC_TEST_READ"] = read
-        logs.append(open(os.path.join(tmp_path, f"rank{r}.err"), "w+"))
-        procs.append(subprocess.Popen(
-            [sys.executable, os.path.join(ROOT, "tests", "rank_worker.py"), name, str(tmp_path),
-             str(steps), json.dumps(xcfg or {}), "1" if host_tokens else "0"], env=env,
-            stderr=logs[-1]))
-    t0 = time.time()
-    while any(p.poll() is None for p in procs):
-        if any(p.poll() not in (None, 0) for p in procs) or time.time() - t0 > timeout:
-            time.sleep(2)  # let the others report, then stop them
-            for p in procs:
-                if p.poll() is None:
-                    p.kill()
-            break
-        time.sleep(0.2)
-    for p in procs:
-        p.wait()
-    errs = []
-    for lg in logs:
-        lg.seek(0)
-        errs.append(lg.read())
-        lg.close()
-    if any(p.returncode != 0 for p in procs):
-        if any("EADDRINUSE" in e for e in errs):
-            raise PortInUse()
-        sys.stderr.write("\n".join(errs))
-    assert all(p.returncode == 0 for p in procs), [p.returncode for p in procs]
-    return [dict(np.load(os.path.join(tmp_path, f"rank{r}.npz"))) for r in range(world)]
-
-
-_ORACLE = {}
-
-
-def oracle_for(name):
-    if name not in _ORACLE:
-        from oracle import numeric as O
-        e = INDEX[name]
-        c = json.load(open(os.path.join(CFG, "clusters", e["cluster"] + ".json")))
-        m = json.load(open(os.path.join(CFG, "models", e["model"] + ".json")))
-        st = O.Step(c, m, open(os.path.join(CFG, "plans", name + ".json")).read())
-        loss, G, W = st.run(0)
-        _ORACLE[name] = (loss, {k: v.copy() for k, v in G.items()},
-                         {k: v.copy() for k, v in W.items()})
-    return _ORACLE[name]
-
-
-def rel(a, b):
-    return float(np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-30))
-
-
-def check_against_oracle(name, ranks):
-    loss, G, W = oracle_for(name)
-    seen = set()
-    for r in ranks:
-        assert abs(float(r["losses"][0]) - loss) <= RTOL * abs(loss), (r["losses"][0], loss)
-        for key in r:
-            if not key.endswith("|grad"):
-                continue
-            t = key[:-5]
-            row0 = int(r[t + "|row0"])
-            g = r[key]
-            ref_g = G[t][row0:row0 + g.shape[0]]
-            ref_w = W[t][row0:row0 + g.shape[0]]
-            assert rel(g, ref_g) < RTOL, (t, rel(g, ref_g))
-            assert rel(r[t + "|w"], ref_w) < RTOL, (t, rel(r[t + "|w"], ref_w))
-            seen.add(t)
-    assert seen == set(G), set(G) - seen  # every tensor is held somewhere
+from parity_util import RTOL, check_against_oracle, oracle_for, rel, run_plan  # noqa: E402
 
 
 @pytest.mark.parametrize("attention", ["fused", "unfused"])
@@ -177,10 +63,12 @@ def test_recompute_matches_stored_activations(tmp_path, name):
                 assert np.allclose(a[key], b[key], rtol=1e-6, atol=1e-7), key
 
 
-@pytest.mark.parametrize("name", ["tiny_pp3_4", "tiny_mixed4"])
+@pytest.mark.parametrize("name", ["tiny_pp3_4", "tiny_mixed4", "tiny_pp3_4_perm"])
 def test_leader_pp_protocol(tmp_path, name):
     """Leader-GPU send -> in-stage broadcast PP hand-off: same
-    step as the direct per-rank hand-off, and parity with the oracle."""
+    step as the direct per-rank hand-off, and parity with the oracle
+    (tiny_pp3_4_perm: the receiving stage's leader is not the lowest world
+    rank of its TP communicator, so the broadcast root must be mapped)."""
     direct = run_plan(name, tmp_path / "direct", steps=2)
     leader = run_plan(name, tmp_path / "leader", steps=2, xcfg={"pp_protocol": "leader"})
     check_against_oracle(name, leader)
