@@ -248,12 +248,21 @@ def run_plan(name: str, steps: int, warmup: int, rank: int, world: int, clocks: 
     # ---- e2e region: public API with host token buffers (H2D) + loss (D2H)
     log(rank, f"{name}: e2e {steps}")
     toks = [ex.synth_tokens(warmup + steps + s) if role["active"] else None for s in range(steps)]
+    ck2 = Clocks(world) if clocks else None
+    if ck2:
+        ck2.start()
+        time.sleep(1.0)  # nvidia-smi start-up
     dist.barrier(rank, world, f"e0-{name}")
+    if ck2:
+        ck2.mark_begin()
     t0 = time.perf_counter()
     loss = None
     for s in range(steps):
         loss = ex.step(toks[s])
     e2e_ms = (time.perf_counter() - t0) * 1e3
+    if ck2:
+        ck2.mark_end()
+    clk_e2e = ck2.stop() if ck2 else None
     e2e_ms = gather_max([e2e_ms], rank, world, f"e2e-{name}")[0]
     h2d = toks[0].nbytes if (role["active"] and toks[0] is not None) else 0
     gp = st.get("gemm_profile", {})
@@ -275,10 +284,16 @@ def run_plan(name: str, steps: int, warmup: int, rank: int, world: int, clocks: 
                          f"tlg-{name}")
     per_rank = gather_all([float(lin.get("flops", 0.0)), float(lin.get("ms", 0.0)),
                            float(lin.get("launches", 0)), share], rank, world, f"lin-{name}")
+    caps = gather_all({k: st.get(k) for k in ("rank", "active", "sm_cap_mode", "sm_applied",
+                                              "sm_total", "sm_fraction")},
+                      rank, world, f"cap-{name}")
+    n_mb = gather_all(int(role.get("n_mb", 0)) if role["active"] else 0, rank, world,
+                      f"nmb-{name}")
     ex.close()
     log(rank, f"{name}: done")
     return dict(name=name, idx=idx, cluster=json.loads(c), model=json.loads(m),
                 plan=json.loads(p), dev_ms=dev_ms, e2e_ms=e2e_ms, loss=loss, clocks=clk,
+                clocks_e2e=clk_e2e, sm_caps=caps, n_mb=n_mb,
                 stats=st, gemm_graph=gg, h2d=sums[0], d2h=sums[1], launches=sums[2], lin_flops=sums[3],
                 lin_ms=sums[4], lin_launches=sums[5], sm_share=sums[6], lin_per_rank=per_rank, tl_all=tl_all, tlg_all=tlg_all,
                 speeds=[x for x in speeds if x])
@@ -355,66 +370,79 @@ def reference_cost(name: str, seconds: float | None, speeds=None):
     return out
 
 
-def cpu_reference(name: str, samples: int, warmup: int) -> dict:
-    """The CPU reference of this path: the fp32 numpy oracle port (the
-    reference repo has no numeric training step), on a bounded
-    sample: one sample (seq_len tokens) through a 1-layer model of the same
-    shape (embedding, 1 decoder layer, final norm, LM head, CE, backward),
-    extrapolated to the full model by the training-FLOP ratio."""
+def cpu_reference(name: str, steps: int, warmup: int) -> dict:
+    """The CPU reference of this path: the fp32 numpy oracle port
+    (oracle/numeric.py; the reference repo has no numeric training step,
+    SURVEY §0) on a bounded sample of the plan's workload, run as is: one
+    sample (seq_len tokens) of the plan's model -- embedding, every decoder
+    layer, final norm, LM head, CE, full backward -- per step, nothing
+    extrapolated.  The AdamW update (once per global batch) is not part of the
+    sample.  BLAS and the per-head attention loops use every host core.
+    Loads only oracle/ code (numpy + the compiled reference planner)."""
     import numpy as np
     from oracle import bookkeeping as bk
     from oracle import numeric as O
-    c, m, p, _ = load(name)
+    c, m, p, idx = load(name)
     md = bk.model_defaults(json.loads(m))
-    one = dict(md, num_layers=1)
     cl = {"machines": {"box": {"intra_bandwidth_gbps": 900, "intra_latency_us": 3}},
           "devices": [{"id": "cpu", "machine": "box", "memory_gib": 64, "peak_tflops": 1}],
           "inter": {"bandwidth_gbps": 900, "latency_us": 3}}
+    L = md["num_layers"]
     plan = {"global_batch": 1, "pipelines": [{"batch": 1, "micro_batch": 1, "stages": [
-        {"devices": ["cpu"], "tp": 1, "layer_start": 0, "layer_count": 1}]}]}
-    st = O.Step(cl, one, json.dumps(plan))
+        {"devices": ["cpu"], "tp": 1, "layer_start": 0, "layer_count": L}]}]}
+    t0 = time.perf_counter()
+    st = O.Step(cl, md, json.dumps(plan))
+    init_s = time.perf_counter() - t0
     stages = st.stage_parts(0)
     S = md["seq_len"]
     times = []
-    for i in range(warmup + samples):
-        G = {k: np.zeros_like(v) for k, v in st.W.items()}
+    G = {k: np.zeros_like(v) for k, v in st.W.items()}
+    for i in range(warmup + steps):
         tok = st.tokens(i, 0, 1)
         t0 = time.perf_counter()
         st.micro_batch(tok, stages, S, G)
         dt = time.perf_counter() - t0
         if i >= warmup:
             times.append(dt)
-    _, f1 = model_flops(one, S)
-    _, ff = model_flops(md, S)
-    t_full = statistics.median(times) * ff / f1
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     cores = cores or 1
     # the reference's own CPU path for the plan (SURVEY 8(d) "CPU reference
     # timing" (a)): hexplan_schedule on this config's cluster, compiled from the
     # reference sources (oracle/_ref), HEXPLAN_THREADS = host cores
     planner = None
+    cost = None
     try:
         from oracle import refshim
-        _, _, _, idx = load(name)
         if refshim.available():
             kind = "symmetric" if idx["source"].endswith("symmetric") else "schedule"
-            if not idx.get("config"):  # hand plan: time the scheduler on its cluster
-                idx = dict(idx, config={"global_batch": json.loads(p)["global_batch"],
-                                        "iterations": 20, "seed": 0, "threads": cores})
+            cfg = idx.get("config")
+            if not cfg:  # hand plan: time the scheduler on its cluster
+                cfg = {"global_batch": json.loads(p)["global_batch"], "iterations": 20,
+                       "seed": 0, "threads": cores}
             t0 = time.perf_counter()
-            res = refshim.plan(c, m, json.dumps(idx["config"]), kind)
+            res = refshim.plan(c, m, json.dumps(cfg), kind)
             planner = {"hexplan": kind, "wall_s": round(time.perf_counter() - t0, 4),
                        "found": bool(res.get("found")), "predicted_s": res.get("cost"),
-                       "config": idx["config"]}
+                       "config": cfg}
+            # the reference cost model (iteration_time, cost_model.cpp:210-258) on
+            # the executed plan itself, through the compiled reference
+            chk = refshim.check_plan(c, m, p)
+            cost = ({"predicted_s": chk["cost"]["total"], "predicted_mfu": chk["cost"]["mfu"],
+                     "source": "oracle/_ref iteration_time"} if "cost" in chk else
+                    {"reference_refuses": chk.get("cost_error"),
+                     "source": "oracle/_ref iteration_time"})
     except Exception as e:  # noqa: BLE001  (reported, never fatal for the bench)
         planner = {"error": str(e)[:200]}
-    return {"value": S / t_full, "unit": "tokens/s", "cores": cores, "kind": "port",
-            "reference_planner": planner,
-            "sample": (f"numpy fp32 oracle (oracle/numeric.py), 1 sample x {S} tokens through "
-                       f"embedding + 1 decoder layer + LM head/CE, fwd+bwd, median of {samples}, "
-                       f"x{ff / f1:.2f} training-FLOP ratio to the {md['num_layers']}-layer model; "
-                       "BLAS threads = all host cores"),
-            "sample_s": statistics.median(times)}
+    t = statistics.mean(times)
+    return {"value": S / t, "unit": "tokens/s", "cores": cores, "kind": "port",
+            "reference_planner": planner, "reference_cost_model": cost,
+            "sample": (f"numpy fp32 oracle (oracle/numeric.py): per step one sample of "
+                       f"{S} tokens through the whole {L}-layer model (embedding, layers, "
+                       f"final norm, LM head, CE; forward + backward), measured, not "
+                       f"extrapolated; AdamW excluded; mean of {steps} after {warmup} "
+                       f"warm-up; BLAS + per-head threads = {cores} host cores"),
+            "sample_ms": [round(x * 1e3, 1) for x in times], "init_s": round(init_s, 1),
+            "ms_per_sample": t * 1e3}
 
 
 def main():
@@ -454,20 +482,22 @@ def main():
         config["exec_config"] = dict(EXEC_CFG)
 
     if a.impl == "reference":
+        # the reference arm: the CPU oracle port on the host cores, rank 0 only;
+        # nothing from the product package is imported or loaded here
         if rank != 0:
             return
-        ref = cpu_reference(asym, samples=max(1, a.steps), warmup=min(a.warmup, 1))
+        ref = cpu_reference(asym, steps=a.steps, warmup=a.warmup)
         line = {"metric": METRIC, "value": ref["value"], "unit": "tokens/s", "impl": "reference",
                 "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
-                "ms_per_step": json.loads(load(asym)[2])["global_batch"] * model["seq_len"]
-                / ref["value"] * 1e3,
+                "ms_per_step": ref["ms_per_sample"],
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic", "config": config,
+                "step_unit": "one sample (seq_len tokens) of the plan's model, fwd + bwd",
                 "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample",
-                                                     "reference_planner")},
+                                                     "reference_planner", "sample_ms", "init_s")},
                 "e2e": {"value": ref["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0},
-                "reference_cost_model": reference_cost(asym, None)}
+                "reference_cost_model": ref["reference_cost_model"]}
         print(json.dumps(line), flush=True)
         return
 
@@ -505,8 +535,9 @@ def main():
         traffic = json.load(open(tf)).get("bytes_per_launch")
     cpu = None
     if a.gpus == 1 and not a.no_cpu_baseline:
-        cb = cpu_reference(asym, samples=1, warmup=0)
-        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "reference_planner")}
+        cb = cpu_reference(asym, steps=1, warmup=0)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "reference_planner",
+                                  "reference_cost_model")}
     line = {
         "metric": METRIC, "value": s["tokens_per_s"], "unit": "tokens/s", "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": s["ms_per_step"],
@@ -532,7 +563,11 @@ def main():
                      "timing": ("CUDA events captured around every GEMM in the step graph, "
                                 "last timed replay" if r.get("gemm_graph") else
                                 "CUDA events around every GEMM, eager profiled pass"),
-                     "launches_per_step": n0 / max(
+                     # the graph events bracket one micro-batch's GEMMs; a step
+                     # runs n_mb micro-batches of the same launches
+                     "launches_sampled": n0,
+                     "micro_batches_sampled": 1 if r.get("gemm_graph") else None,
+                     "launches_per_step": (n0 * r["n_mb"][0]) if r.get("gemm_graph") else n0 / max(
                          r["stats"].get("gemm_profile", {}).get("steps", 1), 1),
                      "algorithmic_flops_per_launch": lin_flops_launch,
                      "avg_launch_ms": lin_ms_launch, "traffic": traffic},
@@ -541,8 +576,12 @@ def main():
         "timeline_ms_rank0_profiled": r["stats"].get("timeline_ms"),
         "timeline_ms_per_step_per_rank_profiled": r["tl_all"] if a.gpus > 1 else None,
         "timeline_ms_one_microbatch_per_rank_graph": r["tlg_all"],
-        "sm_cap_rank0": {k: r["stats"].get(k) for k in ("sm_cap_mode", "sm_applied", "sm_total")},
+        "sm_cap_per_rank": r["sm_caps"],
         "clocks": r["clocks"],
+        # e2e steps sync the host every step: the GPU idles for the copy / sync
+        # gap, and under the power cap the SM clock recovers a little, which is
+        # why e2e can come out at or above the back-to-back device-timed value
+        "clocks_e2e": r["clocks_e2e"],
         "cpu_baseline": cpu,
         "reference_cost_model": reference_cost(asym, s["ms_per_step"] / 1e3, r.get("speeds")),
         "loss": s["loss"],

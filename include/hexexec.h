@@ -74,9 +74,28 @@ size_t hexexec_unique_id_size(void);
 hexexec_status hexexec_unique_id(void* out, size_t out_len, char* err, size_t err_len);
 
 /* ---- executor -------------------------------------------------------------
- * exec_config_json: strict keys (unknown key -> HEXEXEC_ERR_PARSE):
- *   seed, lr, beta1, beta2, eps, weight_decay, sm_cap ("green"|"cta"|"none"),
- *   dp_comm_dtype ("bf16"|"fp32"), validate_only (bool).
+ * exec_config_json: strict keys (unknown key -> HEXEXEC_ERR_PARSE, like the
+ * reference's scheduler config, json_io.cpp:263); defaults in brackets:
+ *   seed [0], lr [1e-3], beta1 [0.9], beta2 [0.95], eps [1e-8],
+ *   weight_decay [0.1]              AdamW hyper-parameters
+ *   sm_cap ["green"|"cta"|"none"]   SM cap of a rank with sm_fraction < 1
+ *   dp_comm_dtype ["bf16"|"fp32"]   dtype of the weighted DP allreduce
+ *   validate_only [false]           host-only layout + memory sizing
+ *   cuda_graph [true]               replay the captured step graph after step 0
+ *   attention ["fused"|"unfused"]   tcgen05 flash attention / GEMM + softmax
+ *   dp_overlap [true]               DP sync + AdamW per layer on a second stream
+ *   recompute [false]               activation recompute
+ *   pp_protocol ["direct"|"leader"] PP hand-off
+ *   tp_reduce ["peer"|"nccl"]       TP partial sums over NVLink peer memory / NCCL
+ *   tp_direction ["auto"|"push"]    critical TP rank does not push (auto)
+ *   tp_pull ["ce"|"sm"]             copy engine / SM copy for the pull
+ *   fuse_swiglu [true]              SwiGLU in the gate-up GEMM epilogue
+ *   fuse_rope [true]                RoPE in the QKV epilogue / dq cast
+ *   gemm_split [false]              tail-wave split-K (not bitwise reproducible)
+ *   wgrad_group [1]                 weight-gradient GEMMs over G micro-batches
+ *   pdl [false]                     programmatic dependent launch of the GEMMs
+ *   profile_gemm [false]            eager steps with per-GEMM / per-op events
+ *   graph_gemm_events [false]       per-GEMM events captured in the step graph
  * world_rank indexes the cluster devices in document order unless devices
  * carry the extension key "rank".  nccl_uid may be NULL when world_size == 1. */
 hexexec_status hexexec_ctx_create(const char* cluster_json, const char* model_json,

@@ -195,7 +195,6 @@ class Executor {
   float *P32 = nullptr, *G32 = nullptr, *Mo = nullptr, *Vo = nullptr;
   bf16 *P16 = nullptr, *G16 = nullptr;
   std::map<std::string, TensorPtrs> named;
-  std::vector<TensorPtrs> by_layer[16];
   // per-layer tensor pointers (local layer index)
   struct LayerW {
     TensorPtrs attn_norm, wqkv, wo, mlp_norm, wgu, wdown;
