@@ -86,6 +86,7 @@ hexexec_status hexexec_unique_id(void* out, size_t out_len, char* err, size_t er
  *   dp_overlap [true]               DP sync + AdamW per layer on a second stream
  *   recompute [false]               activation recompute
  *   pp_protocol ["direct"|"leader"] PP hand-off
+ *   pp_dtype ["bf16"|"fp32"]        PP payload (bf16 = comm_pp_hop's 2 bytes)
  *   tp_reduce ["peer"|"nccl"]       TP partial sums over NVLink peer memory / NCCL
  *   tp_direction ["auto"|"push"]    critical TP rank does not push (auto)
  *   tp_pull ["ce"|"sm"]             copy engine / SM copy for the pull
@@ -145,6 +146,15 @@ hexexec_status hexexec_read_tensor(hexexec_ctx* ctx, const char* name, int which
 /* Per-phase device timings of the last step, kernel-launch counts, memory,
  * SM cap actually applied, communicator sets: JSON, caller frees. */
 char* hexexec_stats_json(const hexexec_ctx* ctx);
+
+/* SM placement of this rank's work (evidence for the SM cap of emulated
+ * tiers): what = 0 launches n probe CTAs on the executor
+ * stream, 1 on its second (DP / comm) stream, 2 runs one persistent GEMM of
+ * the rank's [M, H] x [H, H] shape on the executor stream; every CTA writes
+ * its %smid into sm_ids (n entries; *written = entries filled).  With an
+ * SM-capped rank (green context) every id lies in the rank's partition. */
+hexexec_status hexexec_sm_probe(hexexec_ctx* ctx, int what, int* sm_ids, int n, int* written,
+                                char* err, size_t err_len);
 
 /* ---- kernel-level entry points (device pointers; used by parity tests) --
  * C[z][m,n] = alpha * sum_k A[z][m,k] * B[z][n,k] (+ C if beta); see

@@ -65,6 +65,7 @@ hexexec_tensor_info = _sig("hexexec_tensor_info", _st, _vp, _c, C.POINTER(_i64),
                            C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64))
 hexexec_read_tensor = _sig("hexexec_read_tensor", _st, _vp, _c, _i, _vp, _sz, _c, _sz)
 hexexec_stats_json = _sig("hexexec_stats_json", _vp, _vp)
+hexexec_sm_probe = _sig("hexexec_sm_probe", _st, _vp, _i, _vp, _i, C.POINTER(_i), _c, _sz)
 # kernels
 hexexec_k_gemm = _sig("hexexec_k_gemm", _st, _i, _i, _i, _i, _i, _vp, _i, _i64, _i64, _i64,
                       _vp, _i, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i, _i, _f, _i, _vp)
@@ -102,7 +103,7 @@ EXPORTED = [
     "hexexec_step_async", "hexexec_sync", "hexexec_last_loss", "hexexec_timer",
     "hexexec_set_profile",
     "hexexec_synth_tokens",
-    "hexexec_tensor_info", "hexexec_read_tensor", "hexexec_stats_json", "hexexec_k_gemm", "hexexec_k_gemm_split",
+    "hexexec_tensor_info", "hexexec_read_tensor", "hexexec_stats_json", "hexexec_sm_probe", "hexexec_k_gemm", "hexexec_k_gemm_split",
     "hexexec_k_gemm_peers", "hexexec_k_gemm_raster", "hexexec_k_gemm_sm_limit",
     "hexexec_k_gemm_multicast", "hexexec_k_gemm_tile_auto",
     "hexexec_k_attn_fwd", "hexexec_k_attn_bwd",

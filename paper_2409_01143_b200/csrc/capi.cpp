@@ -271,6 +271,16 @@ hexexec_status hexexec_read_tensor(hexexec_ctx* ctx, const char* name, int which
                  [&] { hexexec::executor_read_tensor(*ctx->ex, name, which, out, n); });
 }
 
+hexexec_status hexexec_sm_probe(hexexec_ctx* ctx, int what, int* sm_ids, int n, int* written,
+                                char* err, size_t err_len) {
+  if (!ctx || !ctx->ex || !sm_ids || !written || what < 0 || what > 2) {
+    set_err(err, err_len, "null argument or bad probe kind");
+    return HEXEXEC_ERR_INVALID;
+  }
+  return guarded(err, err_len,
+                 [&] { *written = hexexec::executor_sm_probe(*ctx->ex, what, sm_ids, n); });
+}
+
 char* hexexec_stats_json(const hexexec_ctx* ctx) {
   if (!ctx || !ctx->ex) return nullptr;
   try {

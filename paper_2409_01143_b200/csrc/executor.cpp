@@ -84,6 +84,7 @@ ExecConfig parse_exec_config(const std::string& text) {
       else if (k == "pdl") c.pdl = v.get<bool>();
       else if (k == "tp_pull") c.tp_pull = v.get<std::string>();
       else if (k == "fuse_rope") c.fuse_rope = v.get<bool>();
+      else if (k == "pp_dtype") c.pp_dtype = v.get<std::string>();
       else throw ParseError("exec config: unknown key '" + k + "'");
     } catch (const nlohmann::json::exception& e) {
       throw ParseError("exec config: bad value for '" + k + "'");
@@ -101,6 +102,8 @@ ExecConfig parse_exec_config(const std::string& text) {
     throw ParseError("exec config: tp_reduce must be peer|nccl");
   if (c.tp_pull != "sm" && c.tp_pull != "ce")
     throw ParseError("exec config: tp_pull must be sm|ce");
+  if (c.pp_dtype != "bf16" && c.pp_dtype != "fp32")
+    throw ParseError("exec config: pp_dtype must be bf16|fp32");
   if (c.tp_direction != "auto" && c.tp_direction != "push")
     throw ParseError("exec config: tp_direction must be auto|push");
   return c;
@@ -214,7 +217,7 @@ class Executor {
   float* gemm_ws_ = nullptr;  // zero between GEMMs (the kernel leaves it zero)
   int* gemm_cnt_ = nullptr;
   float* dg_part_ = nullptr;
-  uint32_t* embed_keys_ = nullptr;
+  void* embed_keys_ = nullptr;
   LayerActs rc_acts_{};  // recompute: the one shared activation set
   int32_t* tokens = nullptr;
   int32_t* tokens_pinned = nullptr;
@@ -348,9 +351,9 @@ class Executor {
       v0 = 64 * role.vocab_chunks.begin;
       mb = role.micro_batch;
       M = mb * S;
-      if (M > 16384)  // embedding-backward sort keys hold 16-bit positions
+      if (M > (int64_t(1) << 30))  // 32-bit row indices in the kernels
         throw LimitExceeded("micro_batch * seq_len = " + std::to_string(M) +
-                            " tokens exceeds the 16384 per micro-batch limit");
+                            " tokens exceeds the per micro-batch limit");
       nl = role.layer_count;
       qkvw = 3 * d * nh;
       kr = d * nh;
@@ -519,6 +522,8 @@ class Executor {
     arena.reserve(M * H * 2);   // ypart
     arena.reserve(M * F * 2 + M * 2 * F * 2 + M * kr * 2 + M * qkvw * 2);
     arena.reserve(M * H * 4 * 2 + M * H * 2 + M * H * 2);  // dx ping-pong, dxb, dy16
+    if (role.stage_count > 1 && cfg.pp_dtype == "bf16")
+      arena.reserve(3 * M * H * 2);                        // PP bf16 send / recv staging
     if (role.last_stage) {
       arena.reserve(M * Vr * 4);  // logits
       arena.reserve(6 * M * 4);   // CE statistics + row losses
@@ -527,7 +532,7 @@ class Executor {
     arena.reserve(kGemmWsBytes);                           // GEMM tail-split workspace
     arena.reserve(kGemmWsCounters * 4);
     arena.reserve(size_t(kRmsBwdCtas) * H * 4);             // rmsnorm bwd partial dg rows
-    arena.reserve(M * 4);                                  // embedding bwd sort keys
+    arena.reserve(embed_bwd_scratch_bytes(int(M)));        // embedding bwd sort keys
     arena.reserve(size_t(S) * size_t(d / 2) * 8);          // RoPE (cos, sin) table
     arena.reserve(role.batch * (S + 1) * 4);               // tokens
     // memory tier: the device's memory_gib caps the rank (cost_model.cpp:130-153
@@ -602,7 +607,7 @@ class Executor {
     gemm_ws_ = arena.take<float>(kGemmWsBytes / 4);
     gemm_cnt_ = arena.take<int>(kGemmWsCounters);
     dg_part_ = arena.take<float>(size_t(kRmsBwdCtas) * H);
-    embed_keys_ = arena.take<uint32_t>(M);
+    embed_keys_ = arena.take<uint8_t>(embed_bwd_scratch_bytes(int(M)));
     rope_tab_ = arena.take<float2>(S * (d / 2));
     k_rope_table(rope_tab_, int(S), int(d), float(L.model.rope_theta), stream);
     ypart = arena.take<bf16>(M * H);
@@ -614,6 +619,11 @@ class Executor {
     dx[1] = arena.take<float>(M * H);
     dxb = arena.take<bf16>(M * H);
     dy16 = arena.take<bf16>(M * H);
+    if (role.stage_count > 1 && cfg.pp_dtype == "bf16") {
+      pp_send16_ = arena.take<bf16>(M * H);
+      pp_rf16_ = arena.take<bf16>(M * H);
+      pp_rb16_ = arena.take<bf16>(M * H);
+    }
     if (role.last_stage) {
       logits = arena.take<float>(M * Vr);
       ce_scr = arena.take<float>(6 * M);
@@ -1420,16 +1430,35 @@ class Executor {
   // leader protocol: only tp_index 0 talks to the neighbouring stage (whose
   // first device is the first entry of the send lists), then broadcasts
   bool pp_leader() const { return cfg.pp_protocol == "leader"; }
+  // pp_dtype "bf16" (default): the hand-off travels as bf16, the 2-byte payload
+  // comm_pp_hop prices (cost_model.cpp:10-13, :59-76); the sender casts its
+  // fp32 stage output / input grad into pp_send16_, the receiver lands it in a
+  // bf16 staging buffer and widens it into the fp32 destination after the
+  // P2P group (and the leader broadcast) completes
+  bool pp16() const { return cfg.pp_dtype == "bf16"; }
   void send_to(const std::vector<int>& peers, const float* buf) {
+    bool cast = false;
     for (size_t k = 0; k < peers.size(); ++k) {
       if (pp_leader() && (role.tp_index != 0 || k > 0)) break;
-      HX_NCCL(ncclSend(buf, size_t(M * H), ncclFloat32, peers[k], world_comm, stream));
+      if (pp16()) {
+        if (!cast) {
+          k_cast_bf16(buf, pp_send16_, M * H, stream);
+          kcheck("pp_cast");
+          cast = true;
+        }
+        HX_NCCL(ncclSend(pp_send16_, size_t(M * H), ncclBfloat16, peers[k], world_comm, stream));
+      } else {
+        HX_NCCL(ncclSend(buf, size_t(M * H), ncclFloat32, peers[k], world_comm, stream));
+      }
       ++nccl_calls_step;
     }
   }
-  void recv_from(int peer, float* buf) {
+  void recv_from(int peer, float* buf, bf16* stage16) {
     if (peer < 0 || (pp_leader() && role.tp_index != 0)) return;
-    HX_NCCL(ncclRecv(buf, size_t(M * H), ncclFloat32, peer, world_comm, stream));
+    if (pp16())
+      HX_NCCL(ncclRecv(stage16, size_t(M * H), ncclBfloat16, peer, world_comm, stream));
+    else
+      HX_NCCL(ncclRecv(buf, size_t(M * H), ncclFloat32, peer, world_comm, stream));
     ++nccl_calls_step;
   }
   // leader protocol, after the receive has completed (outside the P2P group).
@@ -1441,18 +1470,31 @@ class Executor {
     const auto& set = L.comm_sets[size_t(L.tp_comm[size_t(rank)])];
     return int(std::find(set.begin(), set.end(), role.tp_group[0]) - set.begin());
   }
-  void bcast_in_stage(int peer, float* buf) {
-    if (peer < 0 || !pp_leader() || role.tp <= 1) return;
-    HX_NCCL(ncclBroadcast(buf, buf, size_t(M * H), ncclFloat32, leader_comm_rank(), tp_comm(),
-                          stream));
-    ++nccl_calls_step;
+  // after the receive: leader broadcast (leader protocol) and the bf16 -> fp32
+  // widening into the destination
+  void bcast_in_stage(int peer, float* buf, bf16* stage16) {
+    if (peer < 0) return;
+    if (pp_leader() && role.tp > 1) {
+      if (pp16())
+        HX_NCCL(ncclBroadcast(stage16, stage16, size_t(M * H), ncclBfloat16, leader_comm_rank(),
+                              tp_comm(), stream));
+      else
+        HX_NCCL(ncclBroadcast(buf, buf, size_t(M * H), ncclFloat32, leader_comm_rank(),
+                              tp_comm(), stream));
+      ++nccl_calls_step;
+    }
+    if (pp16()) {
+      k_upcast_bf16(stage16, buf, M * H, stream);
+      kcheck("pp_upcast");
+    }
   }
   void send_fwd(Slot& sl) { send_to(role.fwd_send_to, sl.x[size_t(nl)]); }
-  void recv_fwd(Slot& sl) { recv_from(role.fwd_recv_from, sl.x[0]); }
-  void bcast_fwd(Slot& sl) { bcast_in_stage(role.fwd_recv_from, sl.x[0]); }
+  void recv_fwd(Slot& sl) { recv_from(role.fwd_recv_from, sl.x[0], pp_rf16_); }
+  void bcast_fwd(Slot& sl) { bcast_in_stage(role.fwd_recv_from, sl.x[0], pp_rf16_); }
   void send_bwd(const float* g) { send_to(role.bwd_send_to, g); }
-  void recv_bwd(float* g) { recv_from(role.bwd_recv_from, g); }
-  void bcast_bwd(float* g) { bcast_in_stage(role.bwd_recv_from, g); }
+  void recv_bwd(float* g) { recv_from(role.bwd_recv_from, g, pp_rb16_); }
+  void bcast_bwd(float* g) { bcast_in_stage(role.bwd_recv_from, g, pp_rb16_); }
+  bf16 *pp_send16_ = nullptr, *pp_rf16_ = nullptr, *pp_rb16_ = nullptr;
 
   // ------------------------------------------------------------ step
   bool accum_first_ = true;
@@ -2027,6 +2069,54 @@ void executor_read_tensor(Executor& e, const std::string& name, int which, float
 }
 
 std::string executor_stats_json(const Executor& e) { return e.stats(); }
+
+// SM placement of this rank's work (tests of the SM cap): what = 0 a probe
+// kernel of n CTAs on the executor stream, 1 the same on the comm stream,
+// 2 one persistent GEMM of the rank's O-projection shape [M, H] x [H, H] on
+// the executor stream with every CTA logging its %smid (n = its grid, <= n
+// entries written).  out receives the SM ids; returns the entries written.
+int executor_sm_probe(Executor& e, int what, int* out, int n) {
+  if (!e.stream) throw CudaError("executor has no device state (validate_only)");
+  if (n <= 0) return 0;
+  cudaStream_t s = what == 1 ? (e.cstream ? e.cstream : e.stream) : e.stream;
+  int* log = nullptr;
+  HX_CUDA(cudaMalloc(&log, size_t(n) * sizeof(int)));
+  HX_CUDA(cudaMemsetAsync(log, 0xff, size_t(n) * sizeof(int), s));
+  int written = n;
+  if (what == 2) {
+    if (!e.role.active) {
+      cudaFree(log);
+      throw InvalidArgument("sm_probe: idle rank holds no GEMM operands");
+    }
+    // operands: the layer-0 O-projection weight (bf16) as both A rows and B
+    const int64_t Mg = std::min<int64_t>(e.M, 4096), Hh = e.H;
+    bf16* a = nullptr;
+    float* c = nullptr;
+    HX_CUDA(cudaMalloc(&a, size_t(Mg * Hh) * 2));
+    HX_CUDA(cudaMalloc(&c, size_t(Mg * Hh) * 4));
+    HX_CUDA(cudaMemsetAsync(a, 0, size_t(Mg * Hh) * 2, s));
+    GemmDesc g = e.g2(Mg, Hh, Hh, a, 0, Hh, a, 0, Hh, c, Hh, 1);
+    gemm_set_smid_log(log);
+    cudaError_t err = gemm_bf16(g, s);
+    gemm_set_smid_log(nullptr);
+    HX_CUDA(err);
+    HX_CUDA(cudaStreamSynchronize(s));
+    cudaFree(a);
+    cudaFree(c);
+  } else {
+    k_smid_probe(log, n, s);
+    HX_CUDA(cudaGetLastError());
+  }
+  HX_CUDA(cudaMemcpyAsync(out, log, size_t(n) * sizeof(int), cudaMemcpyDeviceToHost, s));
+  HX_CUDA(cudaStreamSynchronize(s));
+  cudaFree(log);
+  if (what == 2) {
+    written = 0;
+    for (int i = 0; i < n; ++i)
+      if (out[i] >= 0) written = i + 1;
+  }
+  return written;
+}
 
 void destroy_executor(Executor* e) { delete e; }
 

@@ -48,6 +48,9 @@ struct ExecConfig {
   // stages' first devices exchange it and the receiving leader broadcasts it
   // over its TP communicator (for links where only leaders are well connected)
   std::string pp_protocol = "direct";
+  // PP payload dtype: "bf16" = the 2-byte hand-off comm_pp_hop prices
+  // (cost_model.cpp:10-13, :59-76); "fp32" = the residual stream as is
+  std::string pp_dtype = "bf16";
   // TP reduction of the row-parallel partials: "peer" = the producing GEMM's
   // epilogue TMA-stores its partial into every TP peer's exchange buffer
   // (IPC-mapped, NVLink) while it runs, a flag handshake orders it, and the
@@ -83,6 +86,7 @@ bool executor_tensor_info(const Executor& e, const std::string& name, int64_t* r
 void executor_read_tensor(Executor& e, const std::string& name, int which, float* out,
                           size_t n);
 std::string executor_stats_json(const Executor& e);
+int executor_sm_probe(Executor& e, int what, int* out, int n);
 void destroy_executor(Executor* e);
 
 }  // namespace hexexec

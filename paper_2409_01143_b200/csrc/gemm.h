@@ -83,6 +83,9 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream);
 
 // number of SMs the GEMM may occupy (0 = all); used for SM-capped ranks
 void gemm_set_sm_limit(int sms);
+// tests: every CTA of later launches writes its %smid to log[blockIdx.x]
+// (null = off); evidence that a capped rank's GEMMs stay in its partition
+void gemm_set_smid_log(int* log);
 // 0 = auto (CTA pairs when M > 128), 1 / 2 = force single-SM / paired tiles
 void gemm_force_cta_group(int cg);
 // grouped tile raster: bands of g M-tiles (default 8); 0 = n fastest

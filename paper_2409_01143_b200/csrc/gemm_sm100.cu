@@ -54,6 +54,7 @@ struct EpiParams {
   int rope_d, rope_S;
   int mc;            // CTA pairs per cluster along N sharing the A tile (TMA multicast)
   int n_tiles_c;     // cluster tiles along N = ceil(n_tiles / mc)
+  int* smid_log;     // tests: CTA b writes its %smid to smid_log[b] (SM-cap placement)
 };
 
 // TMA maps of the peer copies of C (IPC-mapped buffers of the other TP ranks,
@@ -211,6 +212,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  if (p.smid_log != nullptr && threadIdx.x == 0) {
+    uint32_t sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    p.smid_log[blockIdx.x] = int(sm);
+  }
   // cluster = mc CTA pairs along N (pair q owns n-tile mc*nt_c + q); the pair's
   // CTAs are cluster ranks 2q (leader) and 2q+1
   const uint32_t crank_cl = CG == 2 ? cluster_ctarank() : 0;
@@ -687,6 +693,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
 int g_sm_limit = 0;
+int* g_smid_log = nullptr;
 int g_num_sms = 0;
 int g_force_cg = 0;  // 0 = auto, 1 / 2 = force (tests)
 int g_group_m = 8;   // grouped raster band height in M-tiles (0 = n fastest)
@@ -846,6 +853,7 @@ int choose_split(int T, int P, int kblocks, bool direct) {
 }  // namespace
 
 void gemm_set_sm_limit(int sms) { g_sm_limit = sms; }
+void gemm_set_smid_log(int* log) { g_smid_log = log; }
 void gemm_force_cta_group(int cg) { g_force_cg = cg; }
 void gemm_set_group_m(int g) { g_group_m = std::max(0, g); }
 void gemm_set_pdl(int on) { g_pdl = on ? 1 : 0; }
@@ -911,6 +919,7 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t stream) {
   p.mc = (g_mc == 2 && CG == 2 && d.causal == kCausalNone && p.n_tiles >= 2) ? 2 : 1;
   p.n_tiles_c = (p.n_tiles + p.mc - 1) / p.mc;
   p.num_tiles = p.m_tiles * p.n_tiles_c * d.nb1 * d.nb2;
+  p.smid_log = g_smid_log;
   if (d.beta && !d.c_fp32) return cudaErrorInvalidValue;
   CUtensorMap mc, mr;
   if (!make_map_c(&mc, d.C, d.c_fp32, d.N, d.M, d.ldc, d.cbs1, d.cbs2, d.nb1, d.nb2))

@@ -4,6 +4,8 @@
 // the SM count.  Each kernel's HBM bytes and measured GB/s: scripts/bench_ew.py.
 #include <cfloat>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -41,10 +43,75 @@ __global__ void fill_kernel(float* p, bf16* c, long long n, float v) {
   }
 }
 
-__global__ void cast_kernel(const float* in, bf16* out, long long n) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    out[i] = __float2bfloat16_rn(in[i]);
+// fp32 <-> bf16 conversions (PP hand-off, DP gradient prep): 8 elements per
+// thread step, 32-byte fp32 / 16-byte bf16 accesses when both pointers are
+// 16-byte aligned (scalar otherwise); out = bf16(scale * in) / in_bf16 * 1
+__device__ __forceinline__ uint32_t pk2(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+__global__ void cast_kernel(const float* __restrict__ in, bf16* __restrict__ out, long long n,
+                            float scale) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  long long done = 0;
+  if (vec) {
+    const long long n8 = n / 8;
+    for (long long i = t; i < n8; i += stride) {
+      const float4 a = __ldcs(reinterpret_cast<const float4*>(in) + 2 * i);
+      const float4 b = __ldcs(reinterpret_cast<const float4*>(in) + 2 * i + 1);
+      uint4 w;
+      w.x = pk2(a.x * scale, a.y * scale);
+      w.y = pk2(a.z * scale, a.w * scale);
+      w.z = pk2(b.x * scale, b.y * scale);
+      w.w = pk2(b.z * scale, b.w * scale);
+      reinterpret_cast<uint4*>(out)[i] = w;
+    }
+    done = n8 * 8;
+  }
+  for (long long i = done + t; i < n; i += stride) out[i] = __float2bfloat16_rn(in[i] * scale);
+}
+__global__ void upcast_kernel(const bf16* __restrict__ in, float* __restrict__ out, long long n) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  long long done = 0;
+  if (vec) {
+    const long long n8 = n / 8;
+    for (long long i = t; i < n8; i += stride) {
+      const uint4 w = __ldcs(reinterpret_cast<const uint4*>(in) + i);
+      const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+      float f[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        f[2 * k] = __uint_as_float(u[k] << 16);
+        f[2 * k + 1] = __uint_as_float(u[k] & 0xffff0000u);
+      }
+      reinterpret_cast<float4*>(out)[2 * i] = make_float4(f[0], f[1], f[2], f[3]);
+      reinterpret_cast<float4*>(out)[2 * i + 1] = make_float4(f[4], f[5], f[6], f[7]);
+    }
+    done = n8 * 8;
+  }
+  for (long long i = done + t; i < n; i += stride) out[i] = __bfloat162float(in[i]);
+}
+__global__ void scale_kernel(float* g, long long n, float scale) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long done = 0;
+  if ((reinterpret_cast<uintptr_t>(g) & 15) == 0) {
+    const long long n4 = n / 4;
+    for (long long i = t; i < n4; i += stride) {
+      float4 v = reinterpret_cast<float4*>(g)[i];
+      v.x *= scale;
+      v.y *= scale;
+      v.z *= scale;
+      v.w *= scale;
+      reinterpret_cast<float4*>(g)[i] = v;
+    }
+    done = n4 * 4;
+  }
+  for (long long i = done + t; i < n; i += stride) g[i] *= scale;
 }
 
 __global__ void tokens_kernel(int32_t* tok, long long ns, int S1, long long sample0,
@@ -119,6 +186,36 @@ __global__ void embed_segsum_kernel(const uint32_t* __restrict__ keys, const flo
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int r = i; r < end; ++r) {
       const float4 v = *reinterpret_cast<const float4*>(dx + (long long)(keys[r] & 0xffffu) * H + c);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    float4 d = *reinterpret_cast<float4*>(dst + c);
+    d.x += acc.x; d.y += acc.y; d.z += acc.z; d.w += acc.w;
+    *reinterpret_cast<float4*>(dst + c) = d;
+  }
+}
+
+// Large micro-batches (M > kEmbedSortMax tokens): 64-bit (token << 32 | row)
+// keys sorted by a device radix sort (CUB, bits [0, 48): row < 2^32, token <
+// 65536), then the same run sums in row order.
+__global__ void embed_keys64_kernel(const int32_t* tok, int M, int S, unsigned long long* keys) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < M; i += gridDim.x * blockDim.x)
+    keys[i] = ((unsigned long long)uint32_t(tok[(long long)(i / S) * (S + 1) + i % S]) << 32) |
+              unsigned(i);
+}
+
+__global__ void embed_segsum64_kernel(const unsigned long long* __restrict__ keys,
+                                      const float* __restrict__ dx, float* __restrict__ dE, int M,
+                                      int H) {
+  const int i = blockIdx.x;
+  const unsigned long long tk = keys[i] >> 32;
+  if (i > 0 && (keys[i - 1] >> 32) == tk) return;  // not the start of a run
+  int end = i + 1;
+  while (end < M && (keys[end] >> 32) == tk) ++end;
+  float* dst = dE + (long long)tk * H;
+  for (int c = threadIdx.x * 4; c < H; c += blockDim.x * 4) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int r = i; r < end; ++r) {
+      const float4 v = *reinterpret_cast<const float4*>(dx + (long long)(keys[r] & 0xffffffffull) * H + c);
       acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
     }
     float4 d = *reinterpret_cast<float4*>(dst + c);
@@ -683,17 +780,6 @@ __global__ void __launch_bounds__(1024) loss_sum_kernel(const float* __restrict_
 }
 
 // ------------------------------------------------------------------ DP + optimizer
-__global__ void scale_cast_kernel(const float* g, bf16* out, long long n, float scale) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    out[i] = __float2bfloat16_rn(g[i] * scale);
-}
-
-__global__ void scale_kernel(float* g, long long n, float scale) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    g[i] *= scale;
-}
 
 __global__ void adamw_kernel(float* __restrict__ p, bf16* __restrict__ p16, float* __restrict__ m,
                              float* __restrict__ v, const bf16* __restrict__ g16,
@@ -767,7 +853,10 @@ void k_fill(float* p, bf16* copy, long long n, float v, cudaStream_t s) {
   if (n > 0) fill_kernel<<<ew_grid(n, 4), 256, 0, s>>>(p, copy, n, v);
 }
 void k_cast_bf16(const float* in, bf16* out, long long n, cudaStream_t s) {
-  if (n > 0) cast_kernel<<<ew_grid(n, 4), 256, 0, s>>>(in, out, n);
+  if (n > 0) cast_kernel<<<ew_grid(n, 8), 256, 0, s>>>(in, out, n, 1.f);
+}
+void k_upcast_bf16(const bf16* in, float* out, long long n, cudaStream_t s) {
+  if (n > 0) upcast_kernel<<<ew_grid(n, 8), 256, 0, s>>>(in, out, n);
 }
 void k_gen_tokens(int32_t* tok, long long ns, int S, long long sample0, uint64_t seed,
                   long long step, int vocab, cudaStream_t s, const StepParams* sp) {
@@ -824,6 +913,23 @@ void k_peer_copy(void* dst, const void* src, size_t bytes, int sms, cudaStream_t
                                                           static_cast<const uint4*>(src), n16);
 }
 
+// SM placement probe: CTA b records its %smid, holding the SM ~spin_ns so
+// the grid spreads over every SM the stream's context may use
+__global__ void smid_probe_kernel(int* log, long long spin_ns) {
+  if (threadIdx.x != 0) return;
+  uint32_t sm;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  log[blockIdx.x] = int(sm);
+  long long t0, t = 0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < spin_ns);
+}
+void k_smid_probe(int* log, int n, cudaStream_t s) {
+  if (n > 0) smid_probe_kernel<<<n, 32, 0, s>>>(log, 20000);
+}
+
 void k_step_tick(StepParams* sp, float b1, float b2, cudaStream_t s) {
   step_tick_kernel<<<1, 32, 0, s>>>(sp, b1, b2);
 }
@@ -831,9 +937,30 @@ void k_embed_fwd(const int32_t* tok, const float* E, float* x, int M, int S, int
                  cudaStream_t s) {
   if (M > 0) embed_fwd_kernel<<<M, 256, 0, s>>>(tok, E, x, M, S, H);
 }
+size_t embed_bwd_scratch_bytes(int M) {
+  if (M <= kEmbedSortMax) return size_t(M) * 4;
+  size_t temp = 0;
+  if (cub::DeviceRadixSort::SortKeys(nullptr, temp, static_cast<const unsigned long long*>(nullptr),
+                                     static_cast<unsigned long long*>(nullptr), M, 0, 48) !=
+      cudaSuccess) {
+    (void)cudaGetLastError();
+    temp = 2 * size_t(M) * 8 + (size_t(1) << 20);  // no device (host-only sizing): upper bound
+  }
+  return 2 * size_t(M) * 8 + (temp + 255) / 256 * 256;
+}
 void k_embed_bwd(const int32_t* tok, const float* dx, float* dE, int M, int S, int H,
-                 uint32_t* keys, cudaStream_t s) {
+                 void* scratch, cudaStream_t s) {
   if (M <= 0) return;
+  if (M > kEmbedSortMax) {
+    auto* kin = static_cast<unsigned long long*>(scratch);
+    auto* kout = kin + M;
+    size_t temp = embed_bwd_scratch_bytes(M) - 2 * size_t(M) * 8;
+    embed_keys64_kernel<<<ew_grid(M, 4), 256, 0, s>>>(tok, M, S, kin);
+    cub::DeviceRadixSort::SortKeys(static_cast<void*>(kout + M), temp, kin, kout, M, 0, 48, s);
+    embed_segsum64_kernel<<<M, 256, 0, s>>>(kout, dx, dE, M, H);
+    return;
+  }
+  uint32_t* keys = static_cast<uint32_t*>(scratch);
   int n = 1;
   while (n < M) n <<= 1;
   static bool attr = false;
@@ -951,7 +1078,7 @@ void k_ce_finish(const float* logits, int Vr, int v0, const int32_t* tok, int M,
   if (v0 == 0) loss_sum_kernel<<<1, 1024, 0, s>>>(row_loss, M, loss_acc);
 }
 void k_scale_cast(const float* g, bf16* out, long long n, float scale, cudaStream_t s) {
-  if (n > 0) scale_cast_kernel<<<ew_grid(n, 4), 256, 0, s>>>(g, out, n, scale);
+  if (n > 0) cast_kernel<<<ew_grid(n, 8), 256, 0, s>>>(g, out, n, scale);
 }
 void k_scale(float* g, long long n, float scale, cudaStream_t s) {
   if (n > 0) scale_kernel<<<ew_grid(n, 4), 256, 0, s>>>(g, n, scale);

@@ -55,6 +55,7 @@ void k_init_normal(float* master, bf16* copy, long long n, long long global_offs
                    uint64_t tensor_seed, cudaStream_t s);
 void k_fill(float* p, bf16* copy, long long n, float v, cudaStream_t s);
 void k_cast_bf16(const float* in, bf16* out, long long n, cudaStream_t s);
+void k_upcast_bf16(const bf16* in, float* out, long long n, cudaStream_t s);
 // tokens[i][p], i in [0, n_samples), p in [0, S]: sample id = sample0 + i
 // sp != null: step and the gen flag come from the device StepParams
 void k_gen_tokens(int32_t* tok, long long n_samples, int S, long long sample0, uint64_t seed,
@@ -63,10 +64,12 @@ void k_gen_tokens(int32_t* tok, long long n_samples, int S, long long sample0, u
 // x[m, :] = E[tok(m), :]  (tok row stride S+1)
 void k_embed_fwd(const int32_t* tok, const float* E, float* x, int M, int S, int H,
                  cudaStream_t s);
-// dE[tok(m), :] += dx[m, :], deterministic (sorted runs, no atomics); keys:
-// M uint32 scratch; M <= 16384 and position < 65536, token < 65536
+// dE[tok(m), :] += dx[m, :], deterministic (sorted runs, no atomics); token <
+// 65536; scratch of embed_bwd_scratch_bytes(M) (M <= 16384: one-CTA bitonic
+// sort of 32-bit keys; larger micro-batches: device radix sort of 64-bit keys)
+size_t embed_bwd_scratch_bytes(int M);
 void k_embed_bwd(const int32_t* tok, const float* dx, float* dE, int M, int S, int H,
-                 uint32_t* keys, cudaStream_t s);
+                 void* scratch, cudaStream_t s);
 
 // xo = x (+ y[0] + ... + y[ny-1]);  out = bf16(xo * rstd * g);  rstd[m] saved.
 // y slots are ys elements apart (TP partial sums, added in slot order).  xo may
@@ -100,6 +103,8 @@ struct TpPeers {
   int tp, me;
 };
 void k_tp_sync(const TpPeers& p, const StepParams* sp, unsigned op, cudaStream_t s);
+// n CTAs record their %smid into log[0..n) (SM-cap placement evidence)
+void k_smid_probe(int* log, int n, cudaStream_t s);
 // dst (local) <- src (peer memory), bytes % 16 == 0; grid of 4 CTAs per SM
 void k_peer_copy(void* dst, const void* src, size_t bytes, int sms, cudaStream_t s);
 

@@ -162,6 +162,16 @@ class Executor:
                                       err, len(err)), err)
         return out
 
+    def sm_probe(self, what: int, n: int) -> np.ndarray:
+        """SM ids used by this rank's work: 0 = probe CTAs on the executor
+        stream, 1 = on the comm stream, 2 = one persistent GEMM's CTAs."""
+        out = np.full(n, -1, np.int32)
+        written = C.c_int(0)
+        err = L.errbuf()
+        L.check(L.hexexec_sm_probe(self._h, what, out.ctypes.data, n, C.byref(written), err,
+                                   len(err)), err)
+        return out[:written.value]
+
     def stats(self) -> dict:
         return json.loads(L.take_string(L.hexexec_stats_json(self._h)) or "{}")
 

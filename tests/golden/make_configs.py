@@ -142,6 +142,9 @@ HAND = {
     # its TP communicator's rank 0 (lowest world rank) is not the stage leader
     "tiny_pp3_4_perm": ("b200_4_tiers", "tiny", plan([pipe(8, 2, [
         stage(["g0"], 0, 2), stage(["g3", "g2"], 2, 1, [3, 1]), stage(["g1"], 3, 1)])], 4)),
+    # one micro-batch of 160 x 128 = 20480 tokens (> 16384: the embedding
+    # backward sorts 64-bit keys with the device radix sort)
+    "tiny_bigmb": ("b200_1", "tiny", plan([pipe(160, 160, [stage(["g0"], 0, 4)])], 4)),
     # N=1 workload: the cfg2 model on one B200
     "llama7b_4l_1gpu": ("b200_1", "llama7b_4l", plan([pipe(8, 1, [stage(["g0"], 0, 4)])], 4)),
     # cfg2: Llama-7B 4-layer block, TP=2 with 3:1 widths, rank 1 capped to 1/3 SMs

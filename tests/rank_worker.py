@@ -41,6 +41,12 @@ def main():
                 res[t["name"] + "|grad"] = ex.read(t["name"], 1)
                 res[t["name"] + "|w"] = ex.read(t["name"], 0)
                 res[t["name"] + "|row0"] = np.int64(t["row0"])
+    if os.environ.get("HEXEXEC_TEST_SMPROBE") and ex.role["active"]:
+        # SM placement of this rank's work after the steps (graph replays done)
+        n = 4 * 148
+        res["smid_stream"] = ex.sm_probe(0, n)
+        res["smid_comm"] = ex.sm_probe(1, n)
+        res["smid_gemm"] = ex.sm_probe(2, n)
     res["losses"] = np.array(losses, np.float64)
     res["stats"] = np.frombuffer(json.dumps(ex.stats()).encode(), np.uint8)
     np.savez(os.path.join(out, f"rank{rank}.npz"), **res)

@@ -179,3 +179,36 @@ def test_rope_epilogue_matches_kernel(tmp_path, name):
         for key in a:
             if key.endswith("|grad"):
                 assert rel(a[key], b[key]) < 1e-3, (key, rel(a[key], b[key]))
+
+
+@pytest.mark.parametrize("name", ["tiny_pp31", "tiny_pp3_4"])
+def test_pp_bf16_handoff(tmp_path, name):
+    """PP activations / input grads cross stages as bf16 (the 2-byte payload
+    comm_pp_hop prices, cost_model.cpp:10-13, :59-76; default) or fp32: both
+    match the oracle and each other to bf16 rounding of the hand-off."""
+    b16 = run_plan(name, tmp_path / "b16", steps=2, xcfg={"pp_dtype": "bf16"})
+    f32 = run_plan(name, tmp_path / "f32", steps=2, xcfg={"pp_dtype": "fp32"})
+    check_against_oracle(name, b16)
+    check_against_oracle(name, f32)
+    for a, b in zip(b16, f32):
+        assert np.allclose(a["losses"], b["losses"], rtol=2e-3), (a["losses"], b["losses"])
+
+
+def test_dp_comm_dtype_bf16_vs_fp32(tmp_path):
+    """The weighted DP allreduce in bf16 (default; half the bytes of
+    comm_dp_layer's payload at B_type = 4) vs fp32 on DP 5:3: both within the
+    oracle tolerance; the reduced gradients differ by bf16 rounding only."""
+    b16 = run_plan("tiny_dp53", tmp_path / "b16", steps=1, xcfg={"dp_comm_dtype": "bf16"})
+    f32 = run_plan("tiny_dp53", tmp_path / "f32", steps=1, xcfg={"dp_comm_dtype": "fp32"})
+    check_against_oracle("tiny_dp53", b16)
+    check_against_oracle("tiny_dp53", f32)
+    for a, b in zip(b16, f32):
+        for key in a:
+            if key.endswith("|grad"):
+                assert rel(a[key], b[key]) < 1e-2, (key, rel(a[key], b[key]))
+
+
+def test_large_micro_batch(tmp_path):
+    """A micro-batch of 20480 tokens (above the one-CTA sort of the embedding
+    backward): the 64-bit-key radix-sort path, against the oracle."""
+    check_against_oracle("tiny_bigmb", run_plan("tiny_bigmb", tmp_path, steps=1))

@@ -46,7 +46,11 @@ def _summary(name, ranks, report, oracle_loss):
 def _check(name, ranks):
     ora = oracle_for(name, keep=False)
     report = {}
-    check_against_oracle(name, ranks, oracle=ora, report=report)
+    try:
+        check_against_oracle(name, ranks, oracle=ora, report=report)
+    finally:
+        print("PARITY-ALL " + name + " " + json.dumps(
+            {t: [round(a, 5), round(b, 5)] for t, (a, b) in sorted(report.items())}))
     _summary(name, ranks, report, ora[0])
 
 
