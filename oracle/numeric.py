@@ -34,6 +34,19 @@ TENSOR_IDS = {"embed": 0, "attn_norm": 1, "wqkv": 2, "wo": 3, "mlp_norm": 4, "wg
               "wdown": 6, "final_norm": 7, "lm_head": 8}
 
 
+def bf16_round(x):
+    """Round fp32 to the nearest bf16 (ties to even), returned as fp32."""
+    x = np.ascontiguousarray(x, dtype=F32)
+    u = x.view(np.uint32)
+    r = ((u + np.uint32(0x7FFF) + ((u >> np.uint32(16)) & np.uint32(1))) & np.uint32(0xFFFF0000))
+    return r.view(F32)
+
+
+def _ident(x):
+    return x
+
+
+
 def _pool() -> ThreadPoolExecutor:
     """Host threads for the per-head attention loops and the weight init (numpy
     releases the GIL inside ufuncs / BLAS, so threads scale on the host cores;
@@ -81,23 +94,31 @@ def init_weights(m: dict, seed: int) -> dict:
     return W
 
 
-def attn_fwd_head(q, k, v, d):
-    """One (sample, head): causal softmax(q k^T / sqrt(d)) v, fp32.  Returns (P, o)."""
+def attn_fwd_head(q, k, v, d, rb=_ident):
+    """One (sample, head): causal softmax(q k^T / sqrt(d)) v, fp32.  Returns (P, o).
+    rb = bf16_round: the un-normalised probabilities enter the PV product as
+    bf16 (the fused kernel's P operand), the row sum stays fp32."""
     S = q.shape[0]
     s = (q @ k.T) / F32(np.sqrt(d))
     s = np.where(np.triu(np.ones((S, S), bool), 1), -np.inf, s)
     s = s - s.max(-1, keepdims=True)
     e = np.exp(s)
-    P = (e / e.sum(-1, keepdims=True)).astype(F32)
-    return P, P @ v
+    l = e.sum(-1, keepdims=True)
+    P = (e / l).astype(F32)
+    if rb is _ident:
+        return P, P @ v
+    return P, (rb(e) @ v) / l
 
 
-def attn_bwd_head(P, q, k, v, dO, d):
-    """Backward of attn_fwd_head: (dq, dk, dv) before the RoPE inverse."""
-    dV = P.T @ dO
+def attn_bwd_head(P, q, k, v, dO, d, rb=_ident, o=None):
+    """Backward of attn_fwd_head: (dq, dk, dv) before the RoPE inverse.
+    rb = bf16_round: delta from the stored bf16 output o, and P / dS enter
+    their products as bf16 (the fused backward's operands)."""
+    Pb = rb(P)
+    dV = Pb.T @ dO
     dP = dO @ v.T
-    Dv = (P * dP).sum(-1, keepdims=True)
-    dS = P * (dP - Dv) / F32(np.sqrt(d))
+    Dv = (P * dP).sum(-1, keepdims=True) if o is None else (dO * o).sum(-1, keepdims=True)
+    dS = rb(P * (dP - Dv) / F32(np.sqrt(d)))
     return dS @ k, dS.T @ q, dV
 
 
@@ -135,12 +156,21 @@ def silu(x):
     return x / (1.0 + np.exp(-x))
 
 
+
 # ---------------------------------------------------------------- model
 class Step:
     """One training step of the whole plan (all pipelines) in fp32."""
 
     def __init__(self, cluster: dict, model: dict, plan_text: str, seed: int = 0,
-                 lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1):
+                 lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1,
+                 bf16_points: bool = False):
+        """bf16_points: fp32 arithmetic, but every tensor the executor keeps in
+        bf16 is rounded to bf16 at the same point (weight copies used by the
+        GEMMs, normed inputs, QKV after RoPE, attention P / dS operands and
+        output, gate/up, SwiGLU output, final-norm output, dlogits, the bf16
+        grads between GEMMs, TP partial sums): the step the executor computes
+        up to accumulation order.  False = the plain fp32 definition."""
+        self.rb = bf16_round if bf16_points else _ident
         self.m = bk.model_defaults(model)
         self.layout = bk.layout(cluster, model, plan_text)
         self.plan = bk.load_plan(plan_text)
@@ -172,42 +202,58 @@ class Step:
         d = H // nh
         eps = m["norm_eps"]
         p = f"layers.{l}."
+        rb, Wb = self.rb, self.Wb
+        tp = len(parts) > 1
         c = {"x": x}
         xn, r1 = rmsnorm(x, W[p + "attn_norm"][0], eps)
+        xn = rb(xn)
         c.update(xn=xn, r1=r1, parts=[])
         y = np.zeros_like(x)
         cos, sin = rope_tables(S, d, m["rope_theta"])
         for (h0, h1), _ in parts:
             nr = h1 - h0
-            qkv = xn @ W[p + "wqkv"][3 * d * h0:3 * d * h1].T            # [M, nr*3*d]
+            qkv = rb(xn @ Wb(p + "wqkv")[3 * d * h0:3 * d * h1].T)       # [M, nr*3*d]
             t = qkv.reshape(mb, S, nr, 3, d).transpose(0, 2, 3, 1, 4)    # [mb, nr, 3, S, d]
-            q = rope(t[:, :, 0], cos, sin)
-            k = rope(t[:, :, 1], cos, sin)
+            q = rb(rope(t[:, :, 0], cos, sin))
+            k = rb(rope(t[:, :, 1], cos, sin))
             v = t[:, :, 2].astype(F32)
             P = np.empty((mb, nr, S, S), F32)
             o = np.empty((mb, nr, S, d), F32)                            # [mb, nr, S, d]
 
             def head(i):
                 b, h = divmod(i, nr)
-                P[b, h], o[b, h] = attn_fwd_head(q[b, h], k[b, h], v[b, h], d)
+                P[b, h], o[b, h] = attn_fwd_head(q[b, h], k[b, h], v[b, h], d, rb)
             with _blas1():
                 list(_pool().map(head, range(mb * nr)))
-            attn = o.transpose(0, 2, 1, 3).reshape(mb * S, nr * d)
-            y += attn @ W[p + "wo"][d * h0:d * h1]
+            attn = rb(o.transpose(0, 2, 1, 3).reshape(mb * S, nr * d))
+            part = attn @ Wb(p + "wo")[d * h0:d * h1]
+            y += rb(part) if tp else part
             c["parts"].append(dict(q=q, k=k, v=v, P=P, attn=attn))
         x_mid = (x + y).astype(F32)
         hn, r2 = rmsnorm(x_mid, W[p + "mlp_norm"][0], eps)
+        hn = rb(hn)
         c.update(x_mid=x_mid, hn=hn, r2=r2, mparts=[])
         y2 = np.zeros_like(x)
         for _, (f0, f1) in parts:
-            gu = hn @ W[p + "wgu"][2 * f0:2 * f1].T
+            gu = rb(hn @ Wb(p + "wgu")[2 * f0:2 * f1].T)
             ch = gu.reshape(-1, (f1 - f0) // 64, 2, 64)
             g = ch[:, :, 0].reshape(-1, f1 - f0)
             u = ch[:, :, 1].reshape(-1, f1 - f0)
-            a = (silu(g) * u).astype(F32)
-            y2 += a @ W[p + "wdown"][f0:f1]
+            a = rb((silu(g) * u).astype(F32))
+            part = a @ Wb(p + "wdown")[f0:f1]
+            y2 += rb(part) if tp else part
             c["mparts"].append(dict(g=g, u=u, a=a))
         return (x_mid + y2).astype(F32), c
+
+    def Wb(self, name):
+        """The weight copy the GEMMs read (bf16 points: the bf16 copy)."""
+        if self.rb is _ident:
+            return self.W[name]
+        if getattr(self, "_wb_src", None) is not self.W:
+            self._wb_src, self._wb = self.W, {}
+        if name not in self._wb:
+            self._wb[name] = bf16_round(self.W[name])
+        return self._wb[name]
 
     def layer_bwd(self, dx_out, l, parts, c, mb, G):
         m, W = self.m, self.W
@@ -215,43 +261,50 @@ class Step:
         d = H // nh
         p = f"layers.{l}."
         cos, sin = rope_tables(S, d, m["rope_theta"])
+        rb, Wb = self.rb, self.Wb
+        bf = rb is not _ident
+        dxo = rb(dx_out)                    # the bf16 copy the GEMMs read
         dhn = np.zeros_like(dx_out)
         for (_, (f0, f1)), mp in zip(parts, c["mparts"]):
-            Wd = W[p + "wdown"][f0:f1]
-            G[p + "wdown"][f0:f1] += mp["a"].T @ dx_out
-            da = dx_out @ Wd.T
+            Wd = Wb(p + "wdown")[f0:f1]
+            G[p + "wdown"][f0:f1] += mp["a"].T @ dxo
+            da = rb(dxo @ Wd.T)
             sg = 1.0 / (1.0 + np.exp(-mp["g"]))
             dg = da * mp["u"] * sg * (1.0 + mp["g"] * (1.0 - sg))
             du = da * mp["g"] * sg
             n = (f1 - f0) // 64
-            dgu = np.stack([dg.reshape(-1, n, 64), du.reshape(-1, n, 64)], 2).reshape(-1, 2 * (f1 - f0))
+            dgu = rb(np.stack([dg.reshape(-1, n, 64), du.reshape(-1, n, 64)], 2)
+                     .reshape(-1, 2 * (f1 - f0)).astype(F32))
             G[p + "wgu"][2 * f0:2 * f1] += dgu.T @ c["hn"]
-            dhn += dgu @ W[p + "wgu"][2 * f0:2 * f1]
+            dhn += rb(dgu @ Wb(p + "wgu")[2 * f0:2 * f1])
         dxm, dg2 = rmsnorm_bwd(dhn.astype(F32), c["x_mid"], c["r2"], W[p + "mlp_norm"][0])
         G[p + "mlp_norm"][0] += dg2
         dx_mid = (dx_out + dxm).astype(F32)
+        dxmb = rb(dx_mid)
         dxn = np.zeros_like(dx_out)
         for ((h0, h1), _), ap in zip(parts, c["parts"]):
             nr = h1 - h0
-            G[p + "wo"][d * h0:d * h1] += ap["attn"].T @ dx_mid
-            dattn = dx_mid @ W[p + "wo"][d * h0:d * h1].T
+            G[p + "wo"][d * h0:d * h1] += ap["attn"].T @ dxmb
+            dattn = rb(dxmb @ Wb(p + "wo")[d * h0:d * h1].T)
             dO = dattn.reshape(mb, S, nr, d).transpose(0, 2, 1, 3)
+            oo = ap["attn"].reshape(mb, S, nr, d).transpose(0, 2, 1, 3) if bf else None
             dq = np.empty((mb, nr, S, d), F32)
             dk = np.empty((mb, nr, S, d), F32)
             dV = np.empty((mb, nr, S, d), F32)
 
-            def head(i, ap=ap, dO=dO, dq=dq, dk=dk, dV=dV):
+            def head(i, ap=ap, dO=dO, dq=dq, dk=dk, dV=dV, oo=oo):
                 b, h = divmod(i, nr)
                 dq[b, h], dk[b, h], dV[b, h] = attn_bwd_head(
                     ap["P"][b, h], ap["q"][b, h], ap["k"][b, h], ap["v"][b, h],
-                    np.ascontiguousarray(dO[b, h]), d)
+                    np.ascontiguousarray(dO[b, h]), d, rb,
+                    None if oo is None else np.ascontiguousarray(oo[b, h]))
             with _blas1():
                 list(_pool().map(head, range(mb * nr)))
-            dq = rope(dq, cos, sin, inverse=True)
-            dk = rope(dk, cos, sin, inverse=True)
-            dqkv = np.stack([dq, dk, dV], 2).transpose(0, 3, 1, 2, 4).reshape(mb * S, nr * 3 * d)
+            dq = rb(rope(rb(dq), cos, sin, inverse=True))
+            dk = rb(rope(rb(dk), cos, sin, inverse=True))
+            dqkv = rb(np.stack([dq, dk, dV], 2).transpose(0, 3, 1, 2, 4).reshape(mb * S, nr * 3 * d))
             G[p + "wqkv"][3 * d * h0:3 * d * h1] += dqkv.T @ c["xn"]
-            dxn += dqkv @ W[p + "wqkv"][3 * d * h0:3 * d * h1]
+            dxn += rb(dqkv @ Wb(p + "wqkv")[3 * d * h0:3 * d * h1])
         dxi, dg1 = rmsnorm_bwd(dxn.astype(F32), c["x"], c["r1"], W[p + "attn_norm"][0])
         G[p + "attn_norm"][0] += dg1
         return (dx_mid + dxi).astype(F32)
@@ -269,8 +322,10 @@ class Step:
                 x, c = self.layer_fwd(x, l, st["parts"], mb)
                 caches.append((l, st["parts"], c))
         last = stages[-1]
+        rb = self.rb
         xf, rf = rmsnorm(x, W["final_norm"][0], m["norm_eps"])
-        logits = np.concatenate([xf @ W["lm_head"][v0:v1].T for v0, v1 in last["vocab"]], -1)
+        xf = rb(xf)
+        logits = np.concatenate([xf @ self.Wb("lm_head")[v0:v1].T for v0, v1 in last["vocab"]], -1)
         mx = logits.max(-1, keepdims=True)
         e = np.exp((logits - mx).astype(np.float64))
         se = e.sum(-1, keepdims=True)
@@ -278,9 +333,14 @@ class Step:
         dl = (e / se).astype(F32)
         dl[np.arange(len(tgt)), tgt] -= 1.0
         dl *= F32(1.0 / count)
+        dl = rb(dl)
         G["lm_head"] += dl.T @ xf
-        dxf = dl @ W["lm_head"]
-        dx, dgf = rmsnorm_bwd(dxf, x, rf, W["final_norm"][0])
+        if len(last["vocab"]) > 1 and rb is not _ident:   # TP partials of the dgrad, bf16
+            dxf = sum(rb(dl[:, v0 - last["vocab"][0][0]:v1 - last["vocab"][0][0]]
+                         @ self.Wb("lm_head")[v0:v1]) for v0, v1 in last["vocab"])
+        else:
+            dxf = rb(dl @ self.Wb("lm_head"))
+        dx, dgf = rmsnorm_bwd(dxf.astype(F32), x, rf, W["final_norm"][0])
         G["final_norm"][0] += dgf
         for l, parts, c in reversed(caches):
             dx = self.layer_bwd(dx, l, parts, c, mb, G)

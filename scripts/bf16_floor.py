@@ -37,10 +37,14 @@ def main():
         p = open(os.path.join(ROOT, "configs", "plans", name + ".json")).read()
         st = O.Step(json.loads(c), json.loads(m), p)
         loss_o, G, _ = st.run(0)
+        stb = O.Step(json.loads(c), json.loads(m), p, bf16_points=True)
+        loss_e, Ge, _ = stb.run(0)
+        del stb
         st2 = O.Step(json.loads(c), json.loads(m), p)  # fresh initial weights
         loss_b, Gb = TR.step_grads(st2, dtype="bf16")
         loss_f, Gf = TR.step_grads(st2, dtype="fp32")
-        out = {"plan": name, "oracle_loss": loss_o, "torch_bf16_loss": loss_b,
+        out = {"plan": name, "oracle_loss": loss_o, "oracle_bf16_points_loss": loss_e,
+               "torch_bf16_loss": loss_b,
                "torch_fp32_loss": loss_f, "variants": []}
         for xc in variants:
             ex = Executor(c, m, p, xc, rank=0, world_size=1, device=0)
@@ -48,15 +52,17 @@ def main():
             rows = {}
             for t in ex.role["tensors"]:
                 g = ex.read(t["name"], 1)
-                rows[t["name"]] = [round(rel(g, G[t["name"]]), 5), round(rel(Gb[t["name"]], G[t["name"]]), 5),
-                                   round(rel(Gf[t["name"]], G[t["name"]]), 7),
-                                   round(rel(g, Gb[t["name"]]), 5)]
+                n = t["name"]
+                rows[n] = [round(rel(g, G[n]), 5), round(rel(Gb[n], G[n]), 5),
+                           round(rel(Gf[n], G[n]), 7), round(rel(g, Gb[n]), 5),
+                           round(rel(g, Ge[n]), 5), round(rel(Ge[n], G[n]), 5)]
             ex.close()
             worst = {k: max(v[i] for v in rows.values()) for i, k in
                      enumerate(["ours_vs_oracle", "torch_bf16_vs_oracle", "torch_fp32_vs_oracle",
-                                "ours_vs_torch_bf16"])}
+                                "ours_vs_torch_bf16", "ours_vs_oracle_bf16_points",
+                                "oracle_bf16_points_vs_oracle"])}
             out["variants"].append({"exec_config": xc, "loss": loss, "worst": worst,
-                                    "per_tensor [ours, torch_bf16, torch_fp32, ours_vs_torch]": rows})
+                                    "per_tensor [ours, torch_bf16, torch_fp32, ours_vs_torch, ours_vs_bf16pts, bf16pts]": rows})
         print("BF16FLOOR " + json.dumps(out), flush=True)
 
 

@@ -100,22 +100,42 @@ def _run_plan(name, tmp_path, steps, xcfg, host_tokens, timeout, read=None, env_
 _ORACLE = {}
 
 
-def oracle_for(name, keep=True):
-    """(loss, reduced grads, updated weights) of step 0 by the fp32 oracle.
-    keep=False: not cached (the large-shape plans hold 3-5 GB per copy)."""
-    if name in _ORACLE:
-        return _ORACLE[name]
+def oracle_step(name, **kw):
     from oracle import numeric as O
     e = INDEX[name]
     c = json.load(open(os.path.join(CFG, "clusters", e["cluster"] + ".json")))
     m = json.load(open(os.path.join(CFG, "models", e["model"] + ".json")))
-    st = O.Step(c, m, open(os.path.join(CFG, "plans", name + ".json")).read())
+    return O.Step(c, m, open(os.path.join(CFG, "plans", name + ".json")).read(), **kw)
+
+
+def oracle_for(name, keep=True, bf16_points=False):
+    """(loss, reduced grads, updated weights) of step 0 by the fp32 oracle
+    (bf16_points: with the executor's bf16 storage points emulated).
+    keep=False: not cached (the large-shape plans hold 3-5 GB per copy)."""
+    key = (name, bf16_points)
+    if key in _ORACLE:
+        return _ORACLE[key]
+    st = oracle_step(name, bf16_points=bf16_points)
     loss, G, W = st.run(0)
     st.mom = st.vel = None
     out = (loss, G, W)
     if keep:
-        _ORACLE[name] = out
+        _ORACLE[key] = out
     return out
+
+
+def torch_floor(name, G, dtype="bf16"):
+    """Per-tensor normwise deviation from the oracle gradients G of the same
+    step in plain PyTorch (tests/torch_bf16_ref.py) on cuda:0: dtype "bf16"
+    = torch.autocast-style bf16 (the bf16 floor), "fp32" = an independent
+    fp32 restatement that pins the oracle.  Returns (loss, {tensor: error})."""
+    import torch_bf16_ref as TR
+    loss, Gt = TR.step_grads(oracle_step(name), dtype=dtype)
+    out = {t: rel(Gt[t], G[t]) for t in G}
+    del Gt
+    import torch
+    torch.cuda.empty_cache()
+    return loss, out
 
 
 def rel(a, b):

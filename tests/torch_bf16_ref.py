@@ -6,7 +6,7 @@ from the fp32 oracle (oracle/numeric.py) at a given shape, so the parity
 tests can state the executor's error next to PyTorch's own bf16 error on the
 same step.  Model math = oracle/numeric.py:
 RMSNorm, rotate-half RoPE, causal MHA, SwiGLU over 64-column gate/up chunks,
-vocab CE (mean over the pipeline's tokens), single pipeline, one device.
+vocab CE (mean over the global batch's tokens), on one device.
 Not product code: only tests/ import it."""
 from __future__ import annotations
 
@@ -14,17 +14,20 @@ import numpy as np
 
 
 def step_grads(st, device="cuda", dtype="bf16"):
-    """fwd + bwd of every micro-batch of pipeline 0 of oracle Step `st`
-    (single pipeline, one stage) in torch; returns (mean loss, {name: fp32
-    gradient of the pipeline-mean loss})."""
+    """fwd + bwd of the global batch of oracle Step `st` in torch on one
+    device; returns (global mean loss, {name: fp32 gradient of the global
+    mean loss} = the oracle's DP-reduced gradient)."""
     import torch
     import torch.nn.functional as F
     m = st.m
     S, H, nh = m["seq_len"], m["hidden_dim"], m["num_heads"]
     d = H // nh
     eps = m["norm_eps"]
+    # every pipeline's gradient is weighted by batch_i / global_batch, so the
+    # reduced gradient is that of the global mean loss: one pass over the
+    # global batch in micro-batches of pipeline 0's size gives the same math
     p = st.plan["pipelines"][0]
-    assert len(st.plan["pipelines"]) == 1
+    B = st.plan["global_batch"]
     P = {k: torch.tensor(v, device=device, requires_grad=True) for k, v in st.W.items()}
     half = d // 2
     inv = st.m["rope_theta"] ** (-2.0 * np.arange(half, dtype=np.float64) / d)
@@ -43,11 +46,11 @@ def step_grads(st, device="cuda", dtype="bf16"):
         return torch.cat([a * cos - b * sin, b * cos + a * sin], -1).to(adt)
 
     L = m["num_layers"]
-    count = p["batch"] * S
-    toks = torch.tensor(st.tokens(0, 0, p["batch"]), device=device, dtype=torch.long)
+    count = B * S
+    toks = torch.tensor(st.tokens(0, 0, B), device=device, dtype=torch.long)
     total = 0.0
-    mbs = p["micro_batch"]
-    for i in range(p["batch"] // mbs):
+    mbs = p["micro_batch"] if B % p["micro_batch"] == 0 else 1
+    for i in range(B // mbs):
         tok = toks[i * mbs:(i + 1) * mbs]
         inp, tgt = tok[:, :S].reshape(-1), tok[:, 1:].reshape(-1)
         x = P["embed"][inp]
