@@ -187,6 +187,10 @@ hexexec_status hexexec_k_gemm_tile_auto(int on);
  * out [mb*S, nh*d] bf16, lse [mb*nh, S] (log2 domain); backward writes
  * dq/dk/dv into dqkv [mb*S, nh*3*d] (delta / dq_acc: fp32 scratch of
  * mb*nh*S and mb*S*nh*d floats). */
+/* kernel variants of later attention calls (process-wide; 0 = unchanged):
+ * fwd 2 = two query tiles per CTA (default), 1 = one; bwd 2 = separate dQ
+ * epilogue warpgroup (default), 1 = softmax warps stream dQ (v1) */
+hexexec_status hexexec_k_attn_variant(int fwd, int bwd);
 hexexec_status hexexec_k_attn_fwd(const void* qkv, void* out, float* lse, int S, int nh, int d,
                                   int mb, float scale, void* stream);
 hexexec_status hexexec_k_attn_bwd(const void* qkv, const void* out, const void* dout,

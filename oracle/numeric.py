@@ -112,13 +112,14 @@ def attn_fwd_head(q, k, v, d, rb=_ident):
 
 def attn_bwd_head(P, q, k, v, dO, d, rb=_ident, o=None):
     """Backward of attn_fwd_head: (dq, dk, dv) before the RoPE inverse.
-    rb = bf16_round: delta from the stored bf16 output o, and P / dS enter
-    their products as bf16 (the fused backward's operands)."""
+    rb = bf16_round: delta from the stored bf16 output o, P / dS enter their
+    products as bf16 (the fused backward's operands) and dS is formed from the
+    bf16 P (the v2 kernel reads P back from shared memory)."""
     Pb = rb(P)
     dV = Pb.T @ dO
     dP = dO @ v.T
     Dv = (P * dP).sum(-1, keepdims=True) if o is None else (dO * o).sum(-1, keepdims=True)
-    dS = rb(P * (dP - Dv) / F32(np.sqrt(d)))
+    dS = rb((Pb if rb is not _ident else P) * (dP - Dv) / F32(np.sqrt(d)))
     return dS @ k, dS.T @ q, dV
 
 

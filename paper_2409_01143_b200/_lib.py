@@ -75,6 +75,7 @@ hexexec_k_gemm_raster = _sig("hexexec_k_gemm_raster", _st, _i)
 hexexec_k_gemm_sm_limit = _sig("hexexec_k_gemm_sm_limit", _st, _i)
 hexexec_k_gemm_multicast = _sig("hexexec_k_gemm_multicast", _st, _i)
 hexexec_k_gemm_tile_auto = _sig("hexexec_k_gemm_tile_auto", _st, _i)
+hexexec_k_attn_variant = _sig("hexexec_k_attn_variant", _st, _i, _i)
 hexexec_k_attn_fwd = _sig("hexexec_k_attn_fwd", _st, _vp, _vp, _vp, _i, _i, _i, _i, _f, _vp)
 hexexec_k_attn_bwd = _sig("hexexec_k_attn_bwd", _st, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i,
                           _i, _i, _f, _vp)
@@ -106,7 +107,7 @@ EXPORTED = [
     "hexexec_tensor_info", "hexexec_read_tensor", "hexexec_stats_json", "hexexec_sm_probe", "hexexec_k_gemm", "hexexec_k_gemm_split",
     "hexexec_k_gemm_peers", "hexexec_k_gemm_raster", "hexexec_k_gemm_sm_limit",
     "hexexec_k_gemm_multicast", "hexexec_k_gemm_tile_auto",
-    "hexexec_k_attn_fwd", "hexexec_k_attn_bwd",
+    "hexexec_k_attn_variant", "hexexec_k_attn_fwd", "hexexec_k_attn_bwd",
     "hexexec_k_rmsnorm_fwd", "hexexec_k_rmsnorm_bwd", "hexexec_k_rope", "hexexec_k_softmax_fwd",
     "hexexec_k_softmax_bwd", "hexexec_k_swiglu_fwd", "hexexec_k_swiglu_bwd", "hexexec_k_ce",
     "hexexec_k_adamw", "hexexec_k_init_normal", "hexexec_k_tokens", "hexexec_k_sync",

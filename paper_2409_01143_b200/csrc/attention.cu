@@ -962,6 +962,368 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   }
 }
 
+// ------------------------------------------------------------------ backward, v2
+// Same transposed formulation as attn_bwd_kernel; the dQ epilogue moves to its
+// own warpgroup so the softmax warps start the next query tile while dQ_t
+// streams out (in v1 the eight softmax warps also read dQ_t out of TMEM, staged
+// it through the P / dS buffer and issued its TMA reduce-adds -- a serial step
+// of every tile):
+//   warps 0-3   TMA producer (w0), MMA issuer (w1), TMEM allocator (w2)
+//   warps 4-11  P^T, dS^T of each query tile (P values computed in registers
+//               while dK_{t-1} / dQ_{t-1} still read the shared P / dS buffer)
+//   warps 12-15 dQ_t: TMEM -> registers -> swizzled smem (two 4 KB buffers per
+//               warp) -> TMA reduce-add into the fp32 dq accumulator; the dP
+//               region (which holds dQ_t) is released after the TMEM loads
+// dO is single-buffered: its slot frees once dP_t and dV_t have read it, long
+// before dP_{t+1} needs the next tile; that pays for the 32 KB of dQ staging.
+// Registers: 128 per thread for every role (512 threads); the softmax warps
+// stream S / P / dS in 32-column chunks and read P back from shared memory
+// for dS, so they fit without spills.
+constexpr int kBwd2Threads = 512;
+
+template <int D>
+struct Bwd2Cfg {
+  static constexpr uint32_t TILE = T * D * 2;
+  static constexpr uint32_t PDS = T * T * 2;
+  static constexpr uint32_t STG = 4 * 2 * 4096;  // 4 warps x 2 x [32 rows][32 fp32]
+  static constexpr uint32_t SMEM = 1024 + 5 * TILE + PDS + STG + 2 * T * 4 + 256;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kBwd2Threads, 1)
+    attn_bwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                     const __grid_constant__ CUtensorMap tmDQ, const BwdParams p) {
+  using C = Bwd2Cfg<D>;
+  constexpr int DA = D / 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + C::TILE;
+  uint8_t* sQ = sV + C::TILE;        // [2]
+  uint8_t* sDO = sQ + 2 * C::TILE;   // [1]
+  uint8_t* sPD = sDO + C::TILE;      // P^T / dS^T
+  uint8_t* sStg = sPD + C::PDS;      // dQ staging
+  float* sLse = reinterpret_cast<float*>(sStg + C::STG);
+  float* sDel = sLse + T;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sDel + T);
+  uint64_t* kv_full = bar;
+  uint64_t* q_full = bar + 1;    // [2]
+  uint64_t* q_empty = bar + 3;   // [2] Q_t read by S_t and dK_t
+  uint64_t* do_full = bar + 5;
+  uint64_t* do_empty = bar + 6;  // dO_t read by dP_t and dV_t
+  uint64_t* s_full = bar + 7;
+  uint64_t* s_read = bar + 8;    // softmax warps hold S_t in registers
+  uint64_t* dp_full = bar + 9;
+  uint64_t* p_full = bar + 10;
+  uint64_t* pds_free = bar + 11;  // dV_t has read P_t: dS_t may overwrite it
+  uint64_t* ds_full = bar + 12;
+  uint64_t* pd_free = bar + 13;   // dK_t, dQ_t have read dS_t: P_{t+1} may overwrite it
+  uint64_t* dq_full = bar + 14;
+  uint64_t* dq_empty = bar + 15;  // dQ_t loaded out of TMEM: dP_{t+1} may overwrite it
+  uint64_t* dkv_full = bar + 16;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 18);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int nt = p.S / T;
+  const int nz = p.mb * p.nh;
+  const int kt = int(blockIdx.x / nz);  // small kt = most query tiles first
+  const int zh = int(blockIdx.x % nz);
+  const int h = zh % p.nh;
+  const int b = zh / p.nh;
+  const int ntiles = nt - kt;
+  constexpr uint32_t cS = 0, cP = 128, cV = 256, cK = 384;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    tma_prefetch(&tmDO);
+    tma_prefetch(&tmDQ);
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+    }
+    mbar_init(do_full, 1);
+    mbar_init(do_empty, 1);
+    mbar_init(s_full, 1);
+    mbar_init(s_read, 8);
+    mbar_init(dp_full, 1);
+    mbar_init(p_full, 8);
+    mbar_init(pds_free, 1);
+    mbar_init(ds_full, 8);
+    mbar_init(pd_free, 1);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_empty, 4);
+    mbar_init(dkv_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp < 4) {
+    if (warp == 0 && lane == 0) {
+      auto load_q = [&](int t) {
+        const int slot = t & 1;
+        mbar_wait(&q_empty[slot], ((t >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[slot], C::TILE);
+        for (int a = 0; a < DA; ++a)
+          tma_load_4d(sQ + slot * C::TILE + a * ATOM, &tmQ, &q_full[slot], a * 64, (kt + t) * T, h, b);
+      };
+      auto load_do = [&](int t) {
+        mbar_wait(do_empty, (t & 1) ^ 1);
+        mbar_arrive_expect_tx(do_full, C::TILE);
+        for (int a = 0; a < DA; ++a)
+          tma_load_4d(sDO + a * ATOM, &tmDO, do_full, a * 64, (kt + t) * T, h, b);
+      };
+      mbar_arrive_expect_tx(kv_full, 2 * C::TILE);
+      for (int a = 0; a < DA; ++a) {
+        tma_load_4d(sK + a * ATOM, &tmK, kv_full, a * 64, kt * T, h, b);
+        tma_load_4d(sV + a * ATOM, &tmV, kv_full, a * 64, kt * T, h, b);
+      }
+      load_q(0);
+      load_do(0);
+      if (ntiles > 1) load_q(1);
+      for (int t = 1; t < ntiles; ++t) {
+        load_do(t);                       // after dV_{t-1}
+        if (t + 1 < ntiles) load_q(t + 1);  // after dK_{t-1}
+      }
+    } else if (warp == 1 && lane == 0) {
+      const uint32_t id_sp = idesc_bf16(T, T, 0, 0);   // K-major x K-major, N = 128 queries
+      const uint32_t id_acc = idesc_bf16(T, D, 0, 1);  // A K-major, B MN-major, N = D
+      const uint32_t id_dq = idesc_bf16(T, D, 1, 1);   // A MN-major (dS view), B MN-major (K view)
+      const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), pd_addr = smem_u32(sPD);
+      const uint32_t do_addr = smem_u32(sDO);
+      mbar_wait(kv_full, 0);
+      mbar_wait(&q_full[0], 0);
+      tc_fence_after();
+#pragma unroll
+      for (int ks = 0; ks < D / 16; ++ks)
+        tc_mma_f16(tbase + cS, kdesc(k_addr, ks), kdesc(smem_u32(sQ), ks), id_sp, ks > 0 ? 1u : 0u);
+      tc_commit(s_full);
+      for (int t = 0; t < ntiles; ++t) {
+        const int slot = t & 1;
+        const uint32_t q_addr = smem_u32(sQ + slot * C::TILE);
+        mbar_wait(do_full, t & 1);
+        mbar_wait(dq_empty, (t & 1) ^ 1);  // dQ_{t-1} loaded out of the dP region
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks)
+          tc_mma_f16(tbase + cP, kdesc(v_addr, ks), kdesc(do_addr, ks), id_sp, ks > 0 ? 1u : 0u);
+        tc_commit(dp_full);
+        mbar_wait(p_full, t & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < T / 16; ++ks)
+          tc_mma_f16(tbase + cV, kdesc(pd_addr, ks), mnview<0>(do_addr, ks), id_acc,
+                     (t > 0 || ks > 0) ? 1u : 0u);
+        tc_commit(pds_free);
+        tc_commit(do_empty);
+        if (t + 1 < ntiles) {
+          const int ns = (t + 1) & 1;
+          mbar_wait(&q_full[ns], ((t + 1) >> 1) & 1);
+          mbar_wait(s_read, t & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int ks = 0; ks < D / 16; ++ks)
+            tc_mma_f16(tbase + cS, kdesc(k_addr, ks), kdesc(smem_u32(sQ + ns * C::TILE), ks), id_sp,
+                       ks > 0 ? 1u : 0u);
+          tc_commit(s_full);
+        }
+        mbar_wait(ds_full, t & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < T / 16; ++ks)
+          tc_mma_f16(tbase + cK, kdesc(pd_addr, ks), mnview<0>(q_addr, ks), id_acc,
+                     (t > 0 || ks > 0) ? 1u : 0u);
+#pragma unroll
+        for (int ks = 0; ks < T / 16; ++ks)
+          tc_mma_f16(tbase + cP, mnview<0>(pd_addr, ks), mnview<0>(k_addr, ks), id_dq,
+                     ks > 0 ? 1u : 0u);
+        tc_commit(dq_full);
+        tc_commit(&q_empty[slot]);
+        tc_commit(pd_free);
+      }
+      tc_commit(dkv_full);
+    }
+  } else if (warp < 12) {
+    const int g = (warp - 4) / 4;
+    const int ew = (warp - 4) % 4;
+    const int tid = threadIdx.x - 128;          // 0..255
+    const int kr = ew * 32 + lane;              // key row within the tile (TMEM lane)
+    const uint32_t lane_off = uint32_t(ew * 32) << 16;
+    const int q0 = g * (T / 2);
+    const long long z0 = ((long long)b * p.nh + h) * p.S + (long long)kt * T;
+    const float* stat_src = tid < T ? p.lse : p.delta;
+    float* stat_dst = tid < T ? sLse : sDel;
+    const int si = tid % T;
+    float nstat = stat_src[z0 + si];
+    for (int t = 0; t < ntiles; ++t) {
+      const int i = kt + t;
+      const bool diag = t == 0;
+      const long long zq = ((long long)b * p.nh + h) * p.S + (long long)i * T;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      stat_dst[si] = nstat;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (t + 1 < ntiles) nstat = stat_src[zq + T + si];
+      // P^T = exp2(S^T * scale_log2 - lse_q) (causal mask on the diagonal
+      // tile), 32 query columns at a time straight into the P / dS buffer once
+      // dK / dQ of the previous tile have read it; S_{t+1} may then overwrite
+      // the S region.  Register budget: 128 per thread (512-thread CTA).
+      mbar_wait(s_full, t & 1);
+      if (t > 0) mbar_wait(pd_free, (t - 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t su[32];
+        tmem_ld_32x32b_x32(tbase + lane_off + cS + uint32_t(q0 + c * 32), su);
+        tmem_ld_wait();
+#pragma unroll
+        for (int q8 = 0; q8 < 4; ++q8) {
+          const int qb = q0 + c * 32 + q8 * 8;
+          const float4 la = *reinterpret_cast<const float4*>(sLse + qb);
+          const float4 lb = *reinterpret_cast<const float4*>(sLse + qb + 4);
+          const float ls[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
+          float pr[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float e = ex2(fmaf(__uint_as_float(su[q8 * 8 + k]), p.scale_log2, -ls[k]));
+            pr[k] = (diag && kr > qb + k) ? 0.f : e;
+          }
+          uint4 w;
+          w.x = pack_bf16x2(pr[0], pr[1]);
+          w.y = pack_bf16x2(pr[2], pr[3]);
+          w.z = pack_bf16x2(pr[4], pr[5]);
+          w.w = pack_bf16x2(pr[6], pr[7]);
+          *reinterpret_cast<uint4*>(sPD + kchunk(kr, qb / 8)) = w;
+        }
+      }
+      tc_fence_before();
+      fence_async_shared();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(s_read);
+        mbar_arrive(p_full);
+      }
+      // dS^T = P^T (dP^T - delta_q) * scale over the bf16 P^T just written
+      // (read back from the buffer), after dV has consumed P^T
+      mbar_wait(dp_full, t & 1);
+      mbar_wait(pds_free, t & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t dv[32];
+        tmem_ld_32x32b_x32(tbase + lane_off + cP + uint32_t(q0 + c * 32), dv);
+        tmem_ld_wait();
+#pragma unroll
+        for (int q8 = 0; q8 < 4; ++q8) {
+          const int qb = q0 + c * 32 + q8 * 8;
+          uint4* cell = reinterpret_cast<uint4*>(sPD + kchunk(kr, qb / 8));
+          const uint4 pw = *cell;
+          const uint32_t pu4[4] = {pw.x, pw.y, pw.z, pw.w};
+          const float4 da = *reinterpret_cast<const float4*>(sDel + qb);
+          const float4 db = *reinterpret_cast<const float4*>(sDel + qb + 4);
+          const float dl[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
+          float ds[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t u = pu4[k / 2];
+            const float pv = __uint_as_float((k & 1) ? (u & 0xffff0000u) : (u << 16));
+            ds[k] = pv * (__uint_as_float(dv[q8 * 8 + k]) - dl[k]) * p.scale;
+          }
+          uint4 w;
+          w.x = pack_bf16x2(ds[0], ds[1]);
+          w.y = pack_bf16x2(ds[2], ds[3]);
+          w.z = pack_bf16x2(ds[4], ds[5]);
+          w.w = pack_bf16x2(ds[6], ds[7]);
+          *cell = w;
+        }
+      }
+      tc_fence_before();
+      fence_async_shared();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ds_full);
+    }
+    // dK, dV of this key tile -> bf16 into the dqkv buffer (this warp: D/2 columns)
+    mbar_wait(dkv_full, 0);
+    tc_fence_after();
+    const long long row = (long long)b * p.S + kt * T + kr;
+    __nv_bfloat16* dst = p.dqkv + row * (3LL * p.nh * D) + (long long)h * 3 * D;
+#pragma unroll
+    for (int part = 0; part < 2; ++part) {
+      const uint32_t col0 = part == 0 ? cK : cV;
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        const int col = g * (D / 2) + c * 32;
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tbase + lane_off + col0 + uint32_t(col), v);
+        tmem_ld_wait();
+        uint4* o = reinterpret_cast<uint4*>(dst + (part + 1) * D + col);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 w;
+          w.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]), __uint_as_float(v[8 * q + 1]));
+          w.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3]));
+          w.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5]));
+          w.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7]));
+          o[q] = w;
+        }
+      }
+    }
+  } else {
+    // dQ epilogue warps: warp 12 + e reads TMEM lanes [32e, 32e + 32) = query rows
+    const int ew = warp - 12;
+    const uint32_t lane_off = uint32_t(ew * 32) << 16;
+    uint8_t* base = sStg + ew * 8192;
+    int chunk = 0;
+    for (int t = 0; t < ntiles; ++t) {
+      const int qrow = (kt + t) * T + ew * 32;
+      mbar_wait(dq_full, t & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c, ++chunk) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tbase + lane_off + cP + uint32_t(c * 32), v);
+        tmem_ld_wait();
+        if (c == D / 32 - 1) {  // dQ_t is out of TMEM: the dP region is free
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(dq_empty);
+        }
+        uint8_t* stg = base + (chunk & 1) * 4096;
+        if (chunk >= 2) {
+          if (lane == 0) bulk_wait_read<1>();  // this buffer's reduce-add (two chunks ago) has read it
+          __syncwarp();
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<float4*>(stg + swz128(lane, q)) =
+              make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                          __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+        fence_async_shared();
+        __syncwarp();
+        if (lane == 0) {
+          tma_reduce_add_4d(&tmDQ, stg, h * D + c * 32, b * p.S + qrow, 0, 0);
+          bulk_commit();
+        }
+      }
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
 // delta[z][q] = sum_e dO[q, e] * O[q, e]  (thread per (row, head))
 template <int D>
 __global__ void attn_delta_kernel(const __nv_bfloat16* __restrict__ o,
@@ -1090,6 +1452,7 @@ __global__ void attn_dq_cast_rope_kernel(const float* __restrict__ dq, __nv_bflo
 
 // ------------------------------------------------------------------ host
 int g_fwd_variant = 2;  // 2 = two query tiles per CTA (ping-pong), 1 = one tile
+int g_bwd_variant = 2;  // 2 = separate dQ epilogue warpgroup, 1 = softmax warps stream dQ
 PFN_cuTensorMapEncodeTiled_v12000 g_enc = nullptr;
 std::once_flag g_enc_once;
 
@@ -1178,6 +1541,9 @@ cudaError_t launch_bwd(const AttnBwdDesc& a, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel<D>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(attn_bwd2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(Bwd2Cfg<D>::SMEM));
+    if (e != cudaSuccess) return e;
     attr = true;
   }
   const long long W = 3LL * a.nh * D;
@@ -1203,7 +1569,10 @@ cudaError_t launch_bwd(const AttnBwdDesc& a, cudaStream_t s) {
   p.scale = a.scale;
   p.scale_log2 = a.scale * 1.4426950408889634f;
   const int grid = (a.S / T) * a.nh * a.mb;
-  attn_bwd_kernel<D><<<grid, kBwdThreads, C::SMEM, s>>>(q, k, v, dO, dq, p);
+  if (g_bwd_variant == 2)
+    attn_bwd2_kernel<D><<<grid, kBwd2Threads, Bwd2Cfg<D>::SMEM, s>>>(q, k, v, dO, dq, p);
+  else
+    attn_bwd_kernel<D><<<grid, kBwdThreads, C::SMEM, s>>>(q, k, v, dO, dq, p);
   if (a.rope)
     attn_dq_cast_rope_kernel<D><<<ew_blocks(M * a.nh * (D / 16)), 256, 0, s>>>(a.dq_acc, a.dqkv, a.rope,
                                                                               M, a.S, a.nh);
@@ -1215,6 +1584,7 @@ cudaError_t launch_bwd(const AttnBwdDesc& a, cudaStream_t s) {
 }  // namespace
 
 void attention_fwd_variant(int v) { g_fwd_variant = v == 1 ? 1 : 2; }
+void attention_bwd_variant(int v) { g_bwd_variant = v == 1 ? 1 : 2; }
 
 cudaError_t attention_fwd(const AttnDesc& a, cudaStream_t s) {
   if (a.S % T != 0 || a.S <= 0) return cudaErrorInvalidValue;

@@ -21,6 +21,8 @@ struct AttnDesc {
 cudaError_t attention_fwd(const AttnDesc& a, cudaStream_t s);
 // 2 (default): two query tiles per CTA with ping-pong softmax warpgroups; 1: one tile
 void attention_fwd_variant(int v);
+// backward: 2 = dQ epilogue on its own warpgroup (default), 1 = the v1 kernel
+void attention_bwd_variant(int v);
 
 struct AttnBwdDesc {
   const __nv_bfloat16* qkv = nullptr;

@@ -373,6 +373,12 @@ hexexec_status hexexec_k_gemm_split(int split, float* ws, size_t ws_bytes, int* 
   return HEXEXEC_OK;
 }
 
+hexexec_status hexexec_k_attn_variant(int fwd, int bwd) {
+  if (fwd) hexexec::attention_fwd_variant(fwd);
+  if (bwd) hexexec::attention_bwd_variant(bwd);
+  return HEXEXEC_OK;
+}
+
 hexexec_status hexexec_k_attn_fwd(const void* qkv, void* out, float* lse, int S, int nh, int d,
                                   int mb, float scale, void* stream) {
   hexexec::AttnDesc a;

@@ -9,7 +9,8 @@ sys.path.insert(0, __file__.rsplit("/scripts/", 1)[0])
 from paper_2409_01143_b200 import _lib as L  # noqa: E402
 
 
-def main(mb=1, S=2048, nh=32, d=128, iters=10):
+def main(mb=1, S=2048, nh=32, d=128, iters=10, variant=2):
+    L.hexexec_k_attn_variant(0, variant)
     torch.manual_seed(0)
     qkv = torch.randn(mb * S, nh * 3 * d, device="cuda").bfloat16()
     out = torch.zeros(mb * S, nh * d, device="cuda", dtype=torch.bfloat16)
@@ -42,8 +43,32 @@ def main(mb=1, S=2048, nh=32, d=128, iters=10):
         torch.cuda.synchronize()
         ms = s.elapsed_time(e) / iters
         res[name] = {"ms": round(ms, 4), "tflops": round(f / ms / 1e9, 1)}
-    print(json.dumps({"shape": [mb, S, nh, d], **res}))
+    # library baseline on the same shape: torch SDPA (cuDNN / flash backends), bf16, causal
+    q, k, v = (torch.randn(mb, nh, S, d, device="cuda", dtype=torch.bfloat16, requires_grad=True)
+               for _ in range(3))
+    go = torch.randn(mb, nh, S, d, device="cuda", dtype=torch.bfloat16)
+    o = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True)
+    o.backward(go)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        o = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True)
+    e.record()
+    torch.cuda.synchronize()
+    tf = s.elapsed_time(e) / iters
+    s.record()
+    for _ in range(iters):
+        o = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True)
+        o.backward(go)
+    e.record()
+    torch.cuda.synchronize()
+    tb = s.elapsed_time(e) / iters - tf
+    res["torch_sdpa"] = {"fwd_ms": round(tf, 4), "fwd_tflops": round(flops / tf / 1e9, 1),
+                         "bwd_ms": round(tb, 4), "bwd_tflops": round(2.5 * flops / tb / 1e9, 1)}
+    print(json.dumps({"shape": [mb, S, nh, d], "bwd_variant": variant, **res}))
 
 
 if __name__ == "__main__":
-    main()
+    for v in (int(a) for a in (sys.argv[1:] or ["2", "1"])):
+        main(variant=v)
