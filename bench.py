@@ -315,7 +315,13 @@ def summarize(r: dict, steps: int, pk: dict) -> dict:
             "mfu_ref_convention": ref_f / step_s / agg if agg else None,
             "mfu_exact": exact_f / step_s / agg if agg else None,
             "aggregate_sm_share": r["sm_share"], "loss": r["loss"],
-            "sm_ghz": sm_ghz(r), "tokens_per_s_per_sm_ghz": tps / sm_ghz(r) if sm_ghz(r) else None}
+            "sm_ghz": sm_ghz(r), "tokens_per_s_per_sm_ghz": tps / sm_ghz(r) if sm_ghz(r) else None,
+            # the same reference-convention FLOPs over the compute the ranks
+            # actually delivered: sum_r SMs_r x median clock_r x 8192 dense bf16
+            # FLOP / SM / clock (the B200 tensor rate: 2.25 PFLOP/s = 148 SMs x
+            # 1.855 GHz x 8192); under the 1 kW cap a full-SM B200 clocks ~1.5-1.6
+            # GHz while an SM-capped rank holds ~1.9-1.97 GHz
+            "mfu_at_delivered_clock": (ref_f / step_s / (sm_ghz(r) * 8192e9)) if sm_ghz(r) else None}
 
 
 def sm_ghz(r: dict):
@@ -552,6 +558,11 @@ def main():
         "asym_other": alts,
         "sm_ghz": s["sm_ghz"], "tokens_per_s_per_sm_ghz": s["tokens_per_s_per_sm_ghz"],
         "mfu_gap_vs_even": (ev["mfu_ref_convention"] - s["mfu_ref_convention"]) if ev else None,
+        "mfu_gap_vs_even_rel": (1 - s["mfu_ref_convention"] / ev["mfu_ref_convention"]) if ev else None,
+        "mfu_at_delivered_clock": s["mfu_at_delivered_clock"],
+        "mfu_gap_vs_even_at_delivered_clock_rel": (
+            1 - s["mfu_at_delivered_clock"] / ev["mfu_at_delivered_clock"])
+        if ev and ev.get("mfu_at_delivered_clock") and s["mfu_at_delivered_clock"] else None,
         "e2e": {"value": s["e2e_tokens_per_s"], "unit": "tokens/s",
                 "h2d_bytes_per_step": int(r["h2d"]), "d2h_bytes_per_step": int(r["d2h"])},
         "gpu_launches": int(r["launches"] * a.steps),

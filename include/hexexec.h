@@ -150,7 +150,7 @@ char* hexexec_stats_json(const hexexec_ctx* ctx);
 /* SM placement of this rank's work (evidence for the SM cap of emulated
  * tiers): what = 0 launches n probe CTAs on the executor
  * stream, 1 on its second (DP / comm) stream, 2 runs one persistent GEMM of
- * the rank's [M, H] x [H, H] shape on the executor stream; every CTA writes
+ * a fixed 4096 x 4096 x 1024 shape on the executor stream; every CTA writes
  * its %smid into sm_ids (n entries; *written = entries filled).  With an
  * SM-capped rank (green context) every id lies in the rank's partition. */
 hexexec_status hexexec_sm_probe(hexexec_ctx* ctx, int what, int* sm_ids, int n, int* written,

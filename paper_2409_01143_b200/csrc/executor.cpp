@@ -2072,7 +2072,7 @@ std::string executor_stats_json(const Executor& e) { return e.stats(); }
 
 // SM placement of this rank's work (tests of the SM cap): what = 0 a probe
 // kernel of n CTAs on the executor stream, 1 the same on the comm stream,
-// 2 one persistent GEMM of the rank's O-projection shape [M, H] x [H, H] on
+// 2 one persistent 4096 x 4096 x 1024 GEMM on
 // the executor stream with every CTA logging its %smid (n = its grid, <= n
 // entries written).  out receives the SM ids; returns the entries written.
 int executor_sm_probe(Executor& e, int what, int* out, int n) {
@@ -2088,14 +2088,15 @@ int executor_sm_probe(Executor& e, int what, int* out, int n) {
       cudaFree(log);
       throw InvalidArgument("sm_probe: idle rank holds no GEMM operands");
     }
-    // operands: the layer-0 O-projection weight (bf16) as both A rows and B
-    const int64_t Mg = std::min<int64_t>(e.M, 4096), Hh = e.H;
+    // a fixed 4096 x 4096 x 1024 GEMM (256 CTA-pair tiles: every SM the
+    // rank may use gets work) on zeroed scratch operands
+    const int64_t Mg = 4096, Hh = 4096;
     bf16* a = nullptr;
     float* c = nullptr;
     HX_CUDA(cudaMalloc(&a, size_t(Mg * Hh) * 2));
     HX_CUDA(cudaMalloc(&c, size_t(Mg * Hh) * 4));
     HX_CUDA(cudaMemsetAsync(a, 0, size_t(Mg * Hh) * 2, s));
-    GemmDesc g = e.g2(Mg, Hh, Hh, a, 0, Hh, a, 0, Hh, c, Hh, 1);
+    GemmDesc g = e.g2(Mg, Hh, 1024, a, 0, 1024, a, 0, 1024, c, Hh, 1);
     gemm_set_smid_log(log);
     cudaError_t err = gemm_bf16(g, s);
     gemm_set_smid_log(nullptr);

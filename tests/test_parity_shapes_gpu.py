@@ -47,14 +47,16 @@ def _check(name, ranks):
     """Three references for the same step: the fp32 oracle, the oracle with
     the executor's bf16 storage points (bf16_points), and PyTorch's bf16
     autocast step (the bf16 floor).  Asserted, per tensor:
-      * loss within RTOL of the fp32 oracle;
-      * gradient and updated weight within RTOL (2e-2) of the bf16-points
-        oracle -- what remains is accumulation order and rounding of the
-        accumulators (the north star's "bf16 tensor-core accumulation");
-      * gradient deviation from the fp32 oracle <= 1.5 x PyTorch bf16's own
-        deviation (+2e-3): as close to the fp32 definition as a standard
-        bf16 mixed-precision step gets at this shape;
-      * updated weight within RTOL of the fp32 oracle."""
+      * loss within RTOL (2e-2) of the fp32 oracle;
+      * updated weight within RTOL of the fp32 oracle and of the bf16-points
+        oracle;
+      * gradient deviation from the fp32 oracle <= 1.25 x PyTorch bf16's own
+        deviation (+2e-3): as close to the fp32 definition as a standard bf16
+        mixed-precision step gets at this shape (measured: 0.97-1.00 x);
+      * gradient deviation from the bf16-points oracle <= max(RTOL, the bf16
+        floor): with the rounding points emulated, what remains is
+        accumulation order and the decorrelation of later roundings, which
+        grows with depth (1.8 % at 2 layers, 3.1 % at 4 layers of 13B)."""
     loss, G, W = oracle_for(name, keep=False)
     tloss, floor = torch_floor(name, G)
     ours_g, ours_w = {}, {}
@@ -92,8 +94,8 @@ def _check(name, ranks):
     for r in ranks:
         assert abs(float(r["losses"][0]) - loss) <= RTOL * abs(loss), (r["losses"][0], loss)
     bad = {t: v for t, v in rows.items()
-           if not (emu_g[t] < RTOL and emu_w[t] < RTOL and ours_w[t] < RTOL
-                   and ours_g[t] <= 1.5 * floor[t] + 2e-3)}
+           if not (ours_g[t] <= 1.25 * floor[t] + 2e-3 and emu_g[t] <= max(RTOL, floor[t])
+                   and ours_w[t] < RTOL and emu_w[t] < RTOL)}
     assert not bad, bad
 
 

@@ -45,7 +45,7 @@ def test_sm_cap_green_context_partition(tmp_path):
     gemm = set(ranks[1]["smid_gemm"].tolist())
     assert len(part) <= applied and len(comm) <= applied, (len(part), len(comm), applied)
     assert comm <= part | comm and len(part | comm) <= applied, (sorted(part), sorted(comm))
-    assert len(gemm) > 0 and gemm <= (part | comm), sorted(gemm - part - comm)
+    assert len(gemm) >= applied * 0.9 and gemm <= (part | comm), (len(gemm), sorted(gemm - part - comm))
     # the partition is actually used (the probe CTAs spread over it)
     assert len(part) >= applied * 0.9, (len(part), applied)
     print("SMCAP " + json.dumps({"rank1_applied": applied, "probe_sms": len(part),
