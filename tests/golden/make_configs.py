@@ -199,6 +199,17 @@ HAND = {
 }
 
 PLANNED = {
+    # planner-emitted plans small enough for oracle parity on 2 / 4 GPUs (the
+    # hierarchical partitioner + scheduler choose the PP / TP / micro-batch shape)
+    "tiny_4_sched": ("b200_4_tiers", "tiny", "schedule",
+                     {"global_batch": 8, "iterations": 30, "seed": 0, "threads": 8,
+                      "state_multiplier": 2.5}),
+    "llama13b_4l_2_sched": ("b200_2_capped", "llama13b_4l_s256", "schedule",
+                            {"global_batch": 6, "iterations": 30, "seed": 0, "threads": 8,
+                             "state_multiplier": 2.5}),
+    "llama13b_4l_4_sched": ("b200_4_tiers", "llama13b_4l_s256", "schedule",
+                            {"global_batch": 8, "iterations": 30, "seed": 0, "threads": 8,
+                             "state_multiplier": 2.5}),
     # cfg3: Llama-7B on 8 B200 tiers; asymmetric DP with uneven micro-batch counts
     "llama7b_8_asym": ("b200_8_onebox", "llama7b", "schedule",
                        {"global_batch": 64, "iterations": 50, "seed": 0, "threads": 8,

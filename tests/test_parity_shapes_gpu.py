@@ -158,3 +158,22 @@ def test_oracle_pinned_by_torch_fp32(name):
                                "worst": max(err.values())}))
     assert abs(tloss - loss) <= 1e-5 * abs(loss), (tloss, loss)
     assert max(err.values()) < 1e-4, err
+
+
+@pytest.mark.parametrize("name", ["tiny_4_sched", "llama13b_4l_2_sched", "llama13b_4l_4_sched"])
+def test_planner_plans_against_oracle(tmp_path, name):
+    """Plans emitted by the reference's own scheduler / hierarchical graph
+    partitioner (hexplan_schedule through oracle/_ref, committed by
+    tests/golden/make_configs.py; scheduler.cpp:139-341, pipeline_layout.cpp:
+    263-321): 4-stage PP of tiny on the [F, F, 1/2, 1/2] tiers; PP 3/1 of the
+    13B layer shape on the capped pair; TP 2 + TP 2 stages (3/1 layers, two
+    micro-batches of 2) on the tiers -- executed and checked like the hand
+    plans."""
+    if ngpu() < world_of(name):
+        pytest.skip(f"needs {world_of(name)} GPUs")
+    ranks = run_plan(name, tmp_path, timeout=1200)
+    if name.startswith("tiny"):
+        from parity_util import check_against_oracle
+        check_against_oracle(name, ranks)
+    else:
+        _check(name, ranks)
