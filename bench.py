@@ -264,6 +264,15 @@ def run_plan(name: str, steps: int, warmup: int, rank: int, world: int, clocks: 
         ck2.mark_end()
     clk_e2e = ck2.stop() if ck2 else None
     e2e_ms = gather_max([e2e_ms], rank, world, f"e2e-{name}")[0]
+    # order check: the same device-timed loop once more after the e2e region
+    # (e2e has come out 0.5-1 % above the device-timed value although it adds
+    # copies and a host sync per step: a second device-timed pass shows how
+    # much of that is position in the run rather than the measurement)
+    dist.barrier(rank, world, f"t1-{name}")
+    ex.timer_start()
+    for _ in range(steps):
+        ex.step_async()
+    dev2_ms = gather_max([ex.timer_stop()], rank, world, f"dev2-{name}")[0]
     h2d = toks[0].nbytes if (role["active"] and toks[0] is not None) else 0
     gp = st.get("gemm_profile", {})
     lin = gp.get("tp_linear", {})
@@ -287,13 +296,13 @@ def run_plan(name: str, steps: int, warmup: int, rank: int, world: int, clocks: 
     caps = gather_all({k: st.get(k) for k in ("rank", "active", "sm_cap_mode", "sm_applied",
                                               "sm_total", "sm_fraction")},
                       rank, world, f"cap-{name}")
-    n_mb = gather_all(int(role.get("n_mb", 0)) if role["active"] else 0, rank, world,
-                      f"nmb-{name}")
+    n_mb = gather_all(int(role.get("num_micro_batches", 0)) if role["active"] else 0, rank,
+                      world, f"nmb-{name}")
     ex.close()
     log(rank, f"{name}: done")
     return dict(name=name, idx=idx, cluster=json.loads(c), model=json.loads(m),
                 plan=json.loads(p), dev_ms=dev_ms, e2e_ms=e2e_ms, loss=loss, clocks=clk,
-                clocks_e2e=clk_e2e, sm_caps=caps, n_mb=n_mb,
+                clocks_e2e=clk_e2e, sm_caps=caps, n_mb=n_mb, dev2_ms=dev2_ms,
                 stats=st, gemm_graph=gg, h2d=sums[0], d2h=sums[1], launches=sums[2], lin_flops=sums[3],
                 lin_ms=sums[4], lin_launches=sums[5], sm_share=sums[6], lin_per_rank=per_rank, tl_all=tl_all, tlg_all=tlg_all,
                 speeds=[x for x in speeds if x])
@@ -593,6 +602,8 @@ def main():
         # gap, and under the power cap the SM clock recovers a little, which is
         # why e2e can come out at or above the back-to-back device-timed value
         "clocks_e2e": r["clocks_e2e"],
+        "value_second_device_pass_after_e2e": (
+            json.loads(load(asym)[2])["global_batch"] * model["seq_len"] * a.steps / (r["dev2_ms"] / 1e3)),
         "cpu_baseline": cpu,
         "reference_cost_model": reference_cost(asym, s["ms_per_step"] / 1e3, r.get("speeds")),
         "loss": s["loss"],
