@@ -977,8 +977,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 // dO is single-buffered: its slot frees once dP_t and dV_t have read it, long
 // before dP_{t+1} needs the next tile; that pays for the 32 KB of dQ staging.
 // Registers: 128 per thread for every role (512 threads); the softmax warps
-// stream S / P / dS in 32-column chunks and read P back from shared memory
-// for dS, so they fit without spills.
+// stream S / dP in 32-column chunks and keep P as bf16 pairs (32 registers),
+// so they fit without spills; P is computed while dK_{t-1} / dQ_{t-1} still
+// read the P / dS buffer and dS is formed from the same bf16 P.
 constexpr int kBwd2Threads = 512;
 
 template <int D>
@@ -1176,8 +1177,8 @@ __global__ void __launch_bounds__(kBwd2Threads, 1)
       // dK / dQ of the previous tile have read it; S_{t+1} may then overwrite
       // the S region.  Register budget: 128 per thread (512-thread CTA).
       mbar_wait(s_full, t & 1);
-      if (t > 0) mbar_wait(pd_free, (t - 1) & 1);
       tc_fence_after();
+      uint32_t pp[T / 4];  // this thread's 64 P values, bf16 pairs
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         uint32_t su[32];
@@ -1195,23 +1196,25 @@ __global__ void __launch_bounds__(kBwd2Threads, 1)
             const float e = ex2(fmaf(__uint_as_float(su[q8 * 8 + k]), p.scale_log2, -ls[k]));
             pr[k] = (diag && kr > qb + k) ? 0.f : e;
           }
-          uint4 w;
-          w.x = pack_bf16x2(pr[0], pr[1]);
-          w.y = pack_bf16x2(pr[2], pr[3]);
-          w.z = pack_bf16x2(pr[4], pr[5]);
-          w.w = pack_bf16x2(pr[6], pr[7]);
-          *reinterpret_cast<uint4*>(sPD + kchunk(kr, qb / 8)) = w;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) pp[c * 16 + q8 * 4 + k] = pack_bf16x2(pr[2 * k], pr[2 * k + 1]);
         }
       }
+      // the S region may take S_{t+1}; the P / dS buffer once dK_{t-1} and
+      // dQ_{t-1} have read dS_{t-1} (the P math above overlapped those MMAs)
       tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_read);
+      if (t > 0) mbar_wait(pd_free, (t - 1) & 1);
+#pragma unroll
+      for (int q8 = 0; q8 < 8; ++q8)
+        *reinterpret_cast<uint4*>(sPD + kchunk(kr, q0 / 8 + q8)) =
+            make_uint4(pp[q8 * 4], pp[q8 * 4 + 1], pp[q8 * 4 + 2], pp[q8 * 4 + 3]);
       fence_async_shared();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(s_read);
-        mbar_arrive(p_full);
-      }
-      // dS^T = P^T (dP^T - delta_q) * scale over the bf16 P^T just written
-      // (read back from the buffer), after dV has consumed P^T
+      if (lane == 0) mbar_arrive(p_full);
+      // dS^T = P^T (dP^T - delta_q) * scale from the bf16 P^T kept in
+      // registers, into the buffer after dV has consumed P^T
       mbar_wait(dp_full, t & 1);
       mbar_wait(pds_free, t & 1);
       tc_fence_after();
@@ -1224,8 +1227,7 @@ __global__ void __launch_bounds__(kBwd2Threads, 1)
         for (int q8 = 0; q8 < 4; ++q8) {
           const int qb = q0 + c * 32 + q8 * 8;
           uint4* cell = reinterpret_cast<uint4*>(sPD + kchunk(kr, qb / 8));
-          const uint4 pw = *cell;
-          const uint32_t pu4[4] = {pw.x, pw.y, pw.z, pw.w};
+          const uint32_t* pu4 = pp + c * 16 + q8 * 4;
           const float4 da = *reinterpret_cast<const float4*>(sDel + qb);
           const float4 db = *reinterpret_cast<const float4*>(sDel + qb + 4);
           const float dl[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
