@@ -1169,7 +1169,7 @@ __global__ void __launch_bounds__(kBwd2Threads, 1)
       const bool diag = t == 0;
       const long long zq = ((long long)b * p.nh + h) * p.S + (long long)i * T;
       asm volatile("bar.sync 1, 256;" ::: "memory");
-      stat_dst[si] = nstat;
+      sts_f32(stat_dst + si, nstat);
       asm volatile("bar.sync 1, 256;" ::: "memory");
       if (t + 1 < ntiles) nstat = stat_src[zq + T + si];
       // P^T = exp2(S^T * scale_log2 - lse_q) (causal mask on the diagonal
@@ -1187,8 +1187,8 @@ __global__ void __launch_bounds__(kBwd2Threads, 1)
 #pragma unroll
         for (int q8 = 0; q8 < 4; ++q8) {
           const int qb = q0 + c * 32 + q8 * 8;
-          const float4 la = *reinterpret_cast<const float4*>(sLse + qb);
-          const float4 lb = *reinterpret_cast<const float4*>(sLse + qb + 4);
+          const float4 la = lds_f4(sLse + qb);
+          const float4 lb = lds_f4(sLse + qb + 4);
           const float ls[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
           float pr[8];
 #pragma unroll
@@ -1208,8 +1208,8 @@ __global__ void __launch_bounds__(kBwd2Threads, 1)
       if (t > 0) mbar_wait(pd_free, (t - 1) & 1);
 #pragma unroll
       for (int q8 = 0; q8 < 8; ++q8)
-        *reinterpret_cast<uint4*>(sPD + kchunk(kr, q0 / 8 + q8)) =
-            make_uint4(pp[q8 * 4], pp[q8 * 4 + 1], pp[q8 * 4 + 2], pp[q8 * 4 + 3]);
+        sts_u4(sPD + kchunk(kr, q0 / 8 + q8),
+               make_uint4(pp[q8 * 4], pp[q8 * 4 + 1], pp[q8 * 4 + 2], pp[q8 * 4 + 3]));
       fence_async_shared();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
@@ -1226,10 +1226,10 @@ __global__ void __launch_bounds__(kBwd2Threads, 1)
 #pragma unroll
         for (int q8 = 0; q8 < 4; ++q8) {
           const int qb = q0 + c * 32 + q8 * 8;
-          uint4* cell = reinterpret_cast<uint4*>(sPD + kchunk(kr, qb / 8));
+          uint8_t* cell = sPD + kchunk(kr, qb / 8);
           const uint32_t* pu4 = pp + c * 16 + q8 * 4;
-          const float4 da = *reinterpret_cast<const float4*>(sDel + qb);
-          const float4 db = *reinterpret_cast<const float4*>(sDel + qb + 4);
+          const float4 da = lds_f4(sDel + qb);
+          const float4 db = lds_f4(sDel + qb + 4);
           const float dl[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
           float ds[8];
 #pragma unroll
@@ -1243,7 +1243,7 @@ __global__ void __launch_bounds__(kBwd2Threads, 1)
           w.y = pack_bf16x2(ds[2], ds[3]);
           w.z = pack_bf16x2(ds[4], ds[5]);
           w.w = pack_bf16x2(ds[6], ds[7]);
-          *cell = w;
+          sts_u4(cell, w);
         }
       }
       tc_fence_before();
@@ -1304,9 +1304,9 @@ __global__ void __launch_bounds__(kBwd2Threads, 1)
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          *reinterpret_cast<float4*>(stg + swz128(lane, q)) =
-              make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                          __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+          sts_f4(stg + swz128(lane, q),
+                 make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                             __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])));
         fence_async_shared();
         __syncwarp();
         if (lane == 0) {
