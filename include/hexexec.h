@@ -188,8 +188,9 @@ hexexec_status hexexec_k_gemm_tile_auto(int on);
  * dq/dk/dv into dqkv [mb*S, nh*3*d] (delta / dq_acc: fp32 scratch of
  * mb*nh*S and mb*S*nh*d floats). */
 /* kernel variants of later attention calls (process-wide; 0 = unchanged):
- * fwd 2 = two query tiles per CTA (default), 1 = one; bwd 2 = separate dQ
- * epilogue warpgroup (default), 1 = softmax warps stream dQ (v1) */
+ * fwd 2 = two query tiles per CTA (default), 1 = one; bwd 3 = P^T kept in
+ * TMEM + separate dQ epilogue warpgroup (default), 2 = dQ epilogue warpgroup
+ * with P^T through shared memory, 1 = softmax warps stream dQ (r01) */
 hexexec_status hexexec_k_attn_variant(int fwd, int bwd);
 hexexec_status hexexec_k_attn_fwd(const void* qkv, void* out, float* lse, int S, int nh, int d,
                                   int mb, float scale, void* stream);

@@ -1326,6 +1326,354 @@ __global__ void __launch_bounds__(kBwd2Threads, 1)
   }
 }
 
+// ------------------------------------------------------------------ backward, v3
+// v2 with P^T kept in tensor memory: the softmax warps write P^T (bf16 pairs)
+// over the S^T columns they have just read (tcgen05.st), and dV_t = P^T dO_t
+// reads its A operand from TMEM.  The shared P / dS buffer then holds only
+// dS^T, so dS_t no longer waits for dV_t to finish reading P_t, and P_t no
+// longer goes through shared memory.  S_{t+1} is issued once dV_t has
+// completed (its commit), since it overwrites the P^T columns.
+constexpr int kBwd3Threads = 512;
+
+template <int D>
+struct Bwd3Cfg {
+  static constexpr uint32_t TILE = T * D * 2;
+  static constexpr uint32_t PDS = T * T * 2;
+  static constexpr uint32_t STG = 4 * 2 * 4096;  // 4 warps x 2 x [32 rows][32 fp32]
+  static constexpr uint32_t SMEM = 1024 + 5 * TILE + PDS + STG + 2 * T * 4 + 256;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kBwd3Threads, 1)
+    attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                     const __grid_constant__ CUtensorMap tmDQ, const BwdParams p) {
+  using C = Bwd3Cfg<D>;
+  constexpr int DA = D / 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + C::TILE;
+  uint8_t* sQ = sV + C::TILE;        // [2]
+  uint8_t* sDO = sQ + 2 * C::TILE;   // [1]
+  uint8_t* sPD = sDO + C::TILE;      // P^T / dS^T
+  uint8_t* sStg = sPD + C::PDS;      // dQ staging
+  float* sLse = reinterpret_cast<float*>(sStg + C::STG);
+  float* sDel = sLse + T;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sDel + T);
+  uint64_t* kv_full = bar;
+  uint64_t* q_full = bar + 1;    // [2]
+  uint64_t* q_empty = bar + 3;   // [2] Q_t read by S_t and dK_t
+  uint64_t* do_full = bar + 5;
+  uint64_t* do_empty = bar + 6;  // dO_t read by dP_t and dV_t
+  uint64_t* s_full = bar + 7;
+  uint64_t* s_read = bar + 8;    // (unused in v3)
+  uint64_t* dp_full = bar + 9;
+  uint64_t* p_full = bar + 10;
+  uint64_t* pds_free = bar + 11;  // dV_t done: S_{t+1} may overwrite the P^T columns
+  uint64_t* ds_full = bar + 12;
+  uint64_t* pd_free = bar + 13;   // dK_t, dQ_t have read dS_t: P_{t+1} may overwrite it
+  uint64_t* dq_full = bar + 14;
+  uint64_t* dq_empty = bar + 15;  // dQ_t loaded out of TMEM: dP_{t+1} may overwrite it
+  uint64_t* dkv_full = bar + 16;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 18);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int nt = p.S / T;
+  const int nz = p.mb * p.nh;
+  const int kt = int(blockIdx.x / nz);  // small kt = most query tiles first
+  const int zh = int(blockIdx.x % nz);
+  const int h = zh % p.nh;
+  const int b = zh / p.nh;
+  const int ntiles = nt - kt;
+  constexpr uint32_t cS = 0, cP = 128, cV = 256, cK = 384;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    tma_prefetch(&tmDO);
+    tma_prefetch(&tmDQ);
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+    }
+    mbar_init(do_full, 1);
+    mbar_init(do_empty, 1);
+    mbar_init(s_full, 1);
+    mbar_init(s_read, 8);
+    mbar_init(dp_full, 1);
+    mbar_init(p_full, 8);
+    mbar_init(pds_free, 1);
+    mbar_init(ds_full, 8);
+    mbar_init(pd_free, 1);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_empty, 4);
+    mbar_init(dkv_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp < 4) {
+    if (warp == 0 && lane == 0) {
+      auto load_q = [&](int t) {
+        const int slot = t & 1;
+        mbar_wait(&q_empty[slot], ((t >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[slot], C::TILE);
+        for (int a = 0; a < DA; ++a)
+          tma_load_4d(sQ + slot * C::TILE + a * ATOM, &tmQ, &q_full[slot], a * 64, (kt + t) * T, h, b);
+      };
+      auto load_do = [&](int t) {
+        mbar_wait(do_empty, (t & 1) ^ 1);
+        mbar_arrive_expect_tx(do_full, C::TILE);
+        for (int a = 0; a < DA; ++a)
+          tma_load_4d(sDO + a * ATOM, &tmDO, do_full, a * 64, (kt + t) * T, h, b);
+      };
+      mbar_arrive_expect_tx(kv_full, 2 * C::TILE);
+      for (int a = 0; a < DA; ++a) {
+        tma_load_4d(sK + a * ATOM, &tmK, kv_full, a * 64, kt * T, h, b);
+        tma_load_4d(sV + a * ATOM, &tmV, kv_full, a * 64, kt * T, h, b);
+      }
+      load_q(0);
+      load_do(0);
+      if (ntiles > 1) load_q(1);
+      for (int t = 1; t < ntiles; ++t) {
+        load_do(t);                       // after dV_{t-1}
+        if (t + 1 < ntiles) load_q(t + 1);  // after dK_{t-1}
+      }
+    } else if (warp == 1 && lane == 0) {
+      const uint32_t id_sp = idesc_bf16(T, T, 0, 0);   // K-major x K-major, N = 128 queries
+      const uint32_t id_acc = idesc_bf16(T, D, 0, 1);  // A K-major, B MN-major, N = D
+      const uint32_t id_dq = idesc_bf16(T, D, 1, 1);   // A MN-major (dS view), B MN-major (K view)
+      const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), pd_addr = smem_u32(sPD);
+      const uint32_t do_addr = smem_u32(sDO);
+      mbar_wait(kv_full, 0);
+      mbar_wait(&q_full[0], 0);
+      tc_fence_after();
+#pragma unroll
+      for (int ks = 0; ks < D / 16; ++ks)
+        tc_mma_f16(tbase + cS, kdesc(k_addr, ks), kdesc(smem_u32(sQ), ks), id_sp, ks > 0 ? 1u : 0u);
+      tc_commit(s_full);
+      for (int t = 0; t < ntiles; ++t) {
+        const int slot = t & 1;
+        const uint32_t q_addr = smem_u32(sQ + slot * C::TILE);
+        mbar_wait(do_full, t & 1);
+        mbar_wait(dq_empty, (t & 1) ^ 1);  // dQ_{t-1} loaded out of the dP region
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks)
+          tc_mma_f16(tbase + cP, kdesc(v_addr, ks), kdesc(do_addr, ks), id_sp, ks > 0 ? 1u : 0u);
+        tc_commit(dp_full);
+        mbar_wait(p_full, t & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < T / 16; ++ks)
+          tc_mma_f16_ts(tbase + cV, tbase + cS + uint32_t(ks * 8), mnview<0>(do_addr, ks), id_acc,
+                        (t > 0 || ks > 0) ? 1u : 0u);
+        tc_commit(pds_free);  // dV_t done: the P^T columns may take S_{t+1}
+        tc_commit(do_empty);
+        if (t + 1 < ntiles) {
+          const int ns = (t + 1) & 1;
+          mbar_wait(&q_full[ns], ((t + 1) >> 1) & 1);
+          mbar_wait(pds_free, t & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int ks = 0; ks < D / 16; ++ks)
+            tc_mma_f16(tbase + cS, kdesc(k_addr, ks), kdesc(smem_u32(sQ + ns * C::TILE), ks), id_sp,
+                       ks > 0 ? 1u : 0u);
+          tc_commit(s_full);
+        }
+        mbar_wait(ds_full, t & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < T / 16; ++ks)
+          tc_mma_f16(tbase + cK, kdesc(pd_addr, ks), mnview<0>(q_addr, ks), id_acc,
+                     (t > 0 || ks > 0) ? 1u : 0u);
+#pragma unroll
+        for (int ks = 0; ks < T / 16; ++ks)
+          tc_mma_f16(tbase + cP, mnview<0>(pd_addr, ks), mnview<0>(k_addr, ks), id_dq,
+                     ks > 0 ? 1u : 0u);
+        tc_commit(dq_full);
+        tc_commit(&q_empty[slot]);
+        tc_commit(pd_free);
+      }
+      tc_commit(dkv_full);
+    }
+  } else if (warp < 12) {
+    const int g = (warp - 4) / 4;
+    const int ew = (warp - 4) % 4;
+    const int tid = threadIdx.x - 128;          // 0..255
+    const int kr = ew * 32 + lane;              // key row within the tile (TMEM lane)
+    const uint32_t lane_off = uint32_t(ew * 32) << 16;
+    const int q0 = g * (T / 2);
+    const long long z0 = ((long long)b * p.nh + h) * p.S + (long long)kt * T;
+    const float* stat_src = tid < T ? p.lse : p.delta;
+    float* stat_dst = tid < T ? sLse : sDel;
+    const int si = tid % T;
+    float nstat = stat_src[z0 + si];
+    for (int t = 0; t < ntiles; ++t) {
+      const int i = kt + t;
+      const bool diag = t == 0;
+      const long long zq = ((long long)b * p.nh + h) * p.S + (long long)i * T;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      sts_f32(stat_dst + si, nstat);
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (t + 1 < ntiles) nstat = stat_src[zq + T + si];
+      // P^T = exp2(S^T * scale_log2 - lse_q) (causal mask on the diagonal
+      // tile), 32 query columns at a time straight into the P / dS buffer once
+      // dK / dQ of the previous tile have read it; S_{t+1} may then overwrite
+      // the S region.  Register budget: 128 per thread (512-thread CTA).
+      mbar_wait(s_full, t & 1);
+      tc_fence_after();
+      uint32_t pp[T / 4];  // this thread's 64 P values, bf16 pairs
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t su[32];
+        tmem_ld_32x32b_x32(tbase + lane_off + cS + uint32_t(q0 + c * 32), su);
+        tmem_ld_wait();
+#pragma unroll
+        for (int q8 = 0; q8 < 4; ++q8) {
+          const int qb = q0 + c * 32 + q8 * 8;
+          const float4 la = lds_f4(sLse + qb);
+          const float4 lb = lds_f4(sLse + qb + 4);
+          const float ls[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
+          float pr[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float e = ex2(fmaf(__uint_as_float(su[q8 * 8 + k]), p.scale_log2, -ls[k]));
+            pr[k] = (diag && kr > qb + k) ? 0.f : e;
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) pp[c * 16 + q8 * 4 + k] = pack_bf16x2(pr[2 * k], pr[2 * k + 1]);
+        }
+      }
+      // P^T (bf16 pairs, K-major: packed column j = queries 2j, 2j + 1) over
+      // the S^T columns [0, 64) once all eight warps have read their S^T
+      asm volatile("bar.sync 2, 256;" ::: "memory");
+      tmem_st_32x32b_x32(tbase + lane_off + cS + uint32_t(q0 / 2), pp);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+      // dS^T = P^T (dP^T - delta_q) * scale from the bf16 P^T kept in
+      // registers, into the (dS-only) buffer once dK_{t-1} / dQ_{t-1} read it
+      mbar_wait(dp_full, t & 1);
+      if (t > 0) mbar_wait(pd_free, (t - 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t dv[32];
+        tmem_ld_32x32b_x32(tbase + lane_off + cP + uint32_t(q0 + c * 32), dv);
+        tmem_ld_wait();
+#pragma unroll
+        for (int q8 = 0; q8 < 4; ++q8) {
+          const int qb = q0 + c * 32 + q8 * 8;
+          uint8_t* cell = sPD + kchunk(kr, qb / 8);
+          const uint32_t* pu4 = pp + c * 16 + q8 * 4;
+          const float4 da = lds_f4(sDel + qb);
+          const float4 db = lds_f4(sDel + qb + 4);
+          const float dl[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
+          float ds[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t u = pu4[k / 2];
+            const float pv = __uint_as_float((k & 1) ? (u & 0xffff0000u) : (u << 16));
+            ds[k] = pv * (__uint_as_float(dv[q8 * 8 + k]) - dl[k]) * p.scale;
+          }
+          uint4 w;
+          w.x = pack_bf16x2(ds[0], ds[1]);
+          w.y = pack_bf16x2(ds[2], ds[3]);
+          w.z = pack_bf16x2(ds[4], ds[5]);
+          w.w = pack_bf16x2(ds[6], ds[7]);
+          sts_u4(cell, w);
+        }
+      }
+      tc_fence_before();
+      fence_async_shared();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ds_full);
+    }
+    // dK, dV of this key tile -> bf16 into the dqkv buffer (this warp: D/2 columns)
+    mbar_wait(dkv_full, 0);
+    tc_fence_after();
+    const long long row = (long long)b * p.S + kt * T + kr;
+    __nv_bfloat16* dst = p.dqkv + row * (3LL * p.nh * D) + (long long)h * 3 * D;
+#pragma unroll
+    for (int part = 0; part < 2; ++part) {
+      const uint32_t col0 = part == 0 ? cK : cV;
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        const int col = g * (D / 2) + c * 32;
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tbase + lane_off + col0 + uint32_t(col), v);
+        tmem_ld_wait();
+        uint4* o = reinterpret_cast<uint4*>(dst + (part + 1) * D + col);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 w;
+          w.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]), __uint_as_float(v[8 * q + 1]));
+          w.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3]));
+          w.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5]));
+          w.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7]));
+          o[q] = w;
+        }
+      }
+    }
+  } else {
+    // dQ epilogue warps: warp 12 + e reads TMEM lanes [32e, 32e + 32) = query rows
+    const int ew = warp - 12;
+    const uint32_t lane_off = uint32_t(ew * 32) << 16;
+    uint8_t* base = sStg + ew * 8192;
+    int chunk = 0;
+    for (int t = 0; t < ntiles; ++t) {
+      const int qrow = (kt + t) * T + ew * 32;
+      mbar_wait(dq_full, t & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c, ++chunk) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tbase + lane_off + cP + uint32_t(c * 32), v);
+        tmem_ld_wait();
+        if (c == D / 32 - 1) {  // dQ_t is out of TMEM: the dP region is free
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(dq_empty);
+        }
+        uint8_t* stg = base + (chunk & 1) * 4096;
+        if (chunk >= 2) {
+          if (lane == 0) bulk_wait_read<1>();  // this buffer's reduce-add (two chunks ago) has read it
+          __syncwarp();
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          sts_f4(stg + swz128(lane, q),
+                 make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                             __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])));
+        fence_async_shared();
+        __syncwarp();
+        if (lane == 0) {
+          tma_reduce_add_4d(&tmDQ, stg, h * D + c * 32, b * p.S + qrow, 0, 0);
+          bulk_commit();
+        }
+      }
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
 // delta[z][q] = sum_e dO[q, e] * O[q, e]  (thread per (row, head))
 template <int D>
 __global__ void attn_delta_kernel(const __nv_bfloat16* __restrict__ o,
@@ -1355,7 +1703,7 @@ __global__ void attn_delta_kernel(const __nv_bfloat16* __restrict__ o,
 
 // dq (fp32 accumulator [M, nh*D]) -> bf16 q slots of dqkv [M, nh*3*D]
 template <int D>
-__global__ void attn_dq_cast_kernel(const float* __restrict__ dq, __nv_bfloat16* __restrict__ dqkv,
+__global__ void attn_dq_cast_kernel(float* __restrict__ dq, __nv_bfloat16* __restrict__ dqkv,
                                     long long M, int nh) {
   const long long n = M * nh * (D / 8);
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
@@ -1364,8 +1712,10 @@ __global__ void attn_dq_cast_kernel(const float* __restrict__ dq, __nv_bfloat16*
     const long long t = idx / (D / 8);
     const int h = int(t % nh);
     const long long row = t / nh;
-    const float4* src = reinterpret_cast<const float4*>(dq + row * nh * D + h * D + c * 8);
+    float4* src = reinterpret_cast<float4*>(dq + row * nh * D + h * D + c * 8);
     float4 a = src[0], bq = src[1];
+    src[0] = make_float4(0.f, 0.f, 0.f, 0.f);  // leave the accumulator zero
+    src[1] = make_float4(0.f, 0.f, 0.f, 0.f);
     uint4 w;
     w.x = pack_bf16x2(a.x, a.y);
     w.y = pack_bf16x2(a.z, a.w);
@@ -1396,7 +1746,7 @@ __device__ __forceinline__ uint4 f32x8_to_bf16(const float* f) {
   return w;
 }
 template <int D>
-__global__ void attn_dq_cast_rope_kernel(const float* __restrict__ dq, __nv_bfloat16* __restrict__ dqkv,
+__global__ void attn_dq_cast_rope_kernel(float* __restrict__ dq, __nv_bfloat16* __restrict__ dqkv,
                                          const float2* __restrict__ tab, long long M, int S, int nh) {
   constexpr int half = D / 2, g8 = half / 8;
   const long long n = M * nh * g8;
@@ -1416,7 +1766,7 @@ __global__ void attn_dq_cast_rope_kernel(const float* __restrict__ dq, __nv_bflo
       cs[2 * k + 1] = v.z;
       sn[2 * k + 1] = -v.w;
     }
-    const float* src = dq + row * nh * D + h * D + c * 8;
+    float* src = dq + row * nh * D + h * D + c * 8;
     __nv_bfloat16* qb = dqkv + row * 3LL * nh * D + (long long)h * 3 * D + c * 8;
     __nv_bfloat16* kb = qb + D;
     float qa[8], qh[8], ka[8], kh[8];
@@ -1424,6 +1774,11 @@ __global__ void attn_dq_cast_rope_kernel(const float* __restrict__ dq, __nv_bflo
       const float4 a0 = reinterpret_cast<const float4*>(src)[0], a1 = reinterpret_cast<const float4*>(src)[1];
       const float4 b0 = reinterpret_cast<const float4*>(src + half)[0];
       const float4 b1 = reinterpret_cast<const float4*>(src + half)[1];
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);  // leave the accumulator zero
+      reinterpret_cast<float4*>(src)[0] = z;
+      reinterpret_cast<float4*>(src)[1] = z;
+      reinterpret_cast<float4*>(src + half)[0] = z;
+      reinterpret_cast<float4*>(src + half)[1] = z;
       const float fa[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
       const float fb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
@@ -1454,7 +1809,9 @@ __global__ void attn_dq_cast_rope_kernel(const float* __restrict__ dq, __nv_bflo
 
 // ------------------------------------------------------------------ host
 int g_fwd_variant = 2;  // 2 = two query tiles per CTA (ping-pong), 1 = one tile
-int g_bwd_variant = 2;  // 2 = separate dQ epilogue warpgroup, 1 = softmax warps stream dQ
+// 3 = P^T in TMEM + dQ epilogue warpgroup, 2 = dQ epilogue warpgroup,
+// 1 = softmax warps stream dQ (r01)
+int g_bwd_variant = 3;
 PFN_cuTensorMapEncodeTiled_v12000 g_enc = nullptr;
 std::once_flag g_enc_once;
 
@@ -1546,6 +1903,9 @@ cudaError_t launch_bwd(const AttnBwdDesc& a, cudaStream_t s) {
     e = cudaFuncSetAttribute(attn_bwd2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(Bwd2Cfg<D>::SMEM));
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(attn_bwd3_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(Bwd3Cfg<D>::SMEM));
+    if (e != cudaSuccess) return e;
     attr = true;
   }
   const long long W = 3LL * a.nh * D;
@@ -1557,8 +1917,10 @@ cudaError_t launch_bwd(const AttnBwdDesc& a, cudaStream_t s) {
       !encode(&dO, a.dout, D, a.S, a.nh, a.mb, (long long)a.nh * D, D, 64, T) ||
       !encode_f32(&dq, a.dq_acc, (long long)a.nh * D, M))
     return cudaErrorInvalidValue;
-  cudaError_t e = cudaMemsetAsync(a.dq_acc, 0, size_t(M) * a.nh * D * sizeof(float), s);
-  if (e != cudaSuccess) return e;
+  if (!a.dq_acc_zero) {
+    cudaError_t e = cudaMemsetAsync(a.dq_acc, 0, size_t(M) * a.nh * D * sizeof(float), s);
+    if (e != cudaSuccess) return e;
+  }
   attn_delta_kernel<D><<<ew_blocks(M * a.nh), 256, 0, s>>>(a.out, a.dout, a.delta, a.S, a.nh, a.mb);
   BwdParams p;
   p.dq_acc = a.dq_acc;
@@ -1571,7 +1933,9 @@ cudaError_t launch_bwd(const AttnBwdDesc& a, cudaStream_t s) {
   p.scale = a.scale;
   p.scale_log2 = a.scale * 1.4426950408889634f;
   const int grid = (a.S / T) * a.nh * a.mb;
-  if (g_bwd_variant == 2)
+  if (g_bwd_variant == 3)
+    attn_bwd3_kernel<D><<<grid, kBwd3Threads, Bwd3Cfg<D>::SMEM, s>>>(q, k, v, dO, dq, p);
+  else if (g_bwd_variant == 2)
     attn_bwd2_kernel<D><<<grid, kBwd2Threads, Bwd2Cfg<D>::SMEM, s>>>(q, k, v, dO, dq, p);
   else
     attn_bwd_kernel<D><<<grid, kBwdThreads, C::SMEM, s>>>(q, k, v, dO, dq, p);
@@ -1586,7 +1950,7 @@ cudaError_t launch_bwd(const AttnBwdDesc& a, cudaStream_t s) {
 }  // namespace
 
 void attention_fwd_variant(int v) { g_fwd_variant = v == 1 ? 1 : 2; }
-void attention_bwd_variant(int v) { g_bwd_variant = v == 1 ? 1 : 2; }
+void attention_bwd_variant(int v) { g_bwd_variant = (v >= 1 && v <= 3) ? v : 3; }
 
 cudaError_t attention_fwd(const AttnDesc& a, cudaStream_t s) {
   if (a.S % T != 0 || a.S <= 0) return cudaErrorInvalidValue;

@@ -21,7 +21,8 @@ struct AttnDesc {
 cudaError_t attention_fwd(const AttnDesc& a, cudaStream_t s);
 // 2 (default): two query tiles per CTA with ping-pong softmax warpgroups; 1: one tile
 void attention_fwd_variant(int v);
-// backward: 2 = dQ epilogue on its own warpgroup (default), 1 = the v1 kernel
+// backward: 3 = P^T in TMEM + dQ epilogue warpgroup (default), 2 = dQ epilogue
+// warpgroup, 1 = the r01 kernel
 void attention_bwd_variant(int v);
 
 struct AttnBwdDesc {
@@ -30,7 +31,9 @@ struct AttnBwdDesc {
   const __nv_bfloat16* dout = nullptr;  // dO [M, nh*d]
   const float* lse = nullptr;
   float* delta = nullptr;               // [mb*nh, S] scratch: rowsum(dO * O)
-  float* dq_acc = nullptr;              // [M, nh*d] fp32 scratch (zeroed here)
+  float* dq_acc = nullptr;              // [M, nh*d] fp32 scratch (zeroed here unless
+                                        // dq_acc_zero; the dq cast leaves it zero)
+  bool dq_acc_zero = false;             // caller guarantees dq_acc is all zero
   __nv_bfloat16* dqkv = nullptr;        // [M, nh*3*d]: dq, dk, dv written in place
   int S = 0, nh = 0, d = 0, mb = 0;
   float scale = 1.f;

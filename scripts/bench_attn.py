@@ -9,7 +9,7 @@ sys.path.insert(0, __file__.rsplit("/scripts/", 1)[0])
 from paper_2409_01143_b200 import _lib as L  # noqa: E402
 
 
-def main(mb=1, S=2048, nh=32, d=128, iters=10, variant=2):
+def main(mb=1, S=2048, nh=32, d=128, iters=10, variant=3):
     L.hexexec_k_attn_variant(0, variant)
     torch.manual_seed(0)
     qkv = torch.randn(mb * S, nh * 3 * d, device="cuda").bfloat16()
@@ -76,5 +76,5 @@ def main(mb=1, S=2048, nh=32, d=128, iters=10, variant=2):
 
 
 if __name__ == "__main__":
-    for v in (int(a) for a in (sys.argv[1:] or ["2", "1"])):
+    for v in (int(a) for a in (sys.argv[1:] or ["3", "2", "1"])):
         main(variant=v)

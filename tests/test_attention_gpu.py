@@ -45,11 +45,11 @@ def test_attention_forward(cuda, mb, S, nh, d):
     assert (lse / math.log2(math.e) - rl).abs().max().item() < 1e-3
 
 
-@pytest.mark.parametrize("variant", [2, 1])
+@pytest.mark.parametrize("variant", [3, 2, 1])
 @pytest.mark.parametrize("mb,S,nh,d", [(1, 256, 2, 128), (2, 384, 3, 64), (1, 2048, 2, 128),
                                        (1, 2048, 32, 128), (1, 128, 1, 64)])
 def test_attention_backward(cuda, mb, S, nh, d, variant):
-    """v2 (dQ epilogue warpgroup, default) and v1 backward kernels."""
+    """v3 (P^T in TMEM), v2 (dQ epilogue warpgroup) and v1 backward kernels."""
     L = _L()
     assert L.hexexec_k_attn_variant(0, variant) == 0
     torch.manual_seed(1)
@@ -72,6 +72,6 @@ def test_attention_backward(cuda, mb, S, nh, d, variant):
     ro.backward(dout.float())
     g = dqkv.float().view(mb * S, nh, 3, d)
     r = x.grad.view(mb * S, nh, 3, d)
-    L.hexexec_k_attn_variant(0, 2)
+    L.hexexec_k_attn_variant(0, 3)
     for part in range(3):
         assert _rel(g[:, :, part], r[:, :, part]) < 2e-2, part
