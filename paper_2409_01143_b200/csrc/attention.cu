@@ -1674,30 +1674,37 @@ __global__ void __launch_bounds__(kBwd3Threads, 1)
   }
 }
 
-// delta[z][q] = sum_e dO[q, e] * O[q, e]  (thread per (row, head))
+// delta[z][q] = sum_e dO[q, e] * O[q, e]: D/8 consecutive threads per (row,
+// head), 16-byte coalesced loads of O and dO, shuffle reduction
 template <int D>
 __global__ void attn_delta_kernel(const __nv_bfloat16* __restrict__ o,
                                   const __nv_bfloat16* __restrict__ dout, float* delta, int S,
                                   int nh, int mb) {
-  const long long n = (long long)mb * S * nh;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+  constexpr int G = D / 8;  // threads per (row, head): 16 (d 128) or 8 (d 64)
+  const long long n = (long long)mb * S * nh * G;
+  const int sub = threadIdx.x % G;
+  // warp-uniform trip count (the shuffles need every lane of the warp)
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx - threadIdx.x % 32 < n;
        idx += (long long)gridDim.x * blockDim.x) {
-    const int h = int(idx % nh);
-    const long long row = idx / nh;  // b*S + s
-    const long long off = row * (long long)nh * D + (long long)h * D;
+    const long long rh = idx / G;  // row * nh + h
     float acc = 0.f;
-#pragma unroll
-    for (int c = 0; c < D / 8; ++c) {
-      uint4 a = reinterpret_cast<const uint4*>(o + off)[c];
-      uint4 g = reinterpret_cast<const uint4*>(dout + off)[c];
+    if (idx < n) {
+      const uint4 a = __ldcs(reinterpret_cast<const uint4*>(o + rh * D) + sub);
+      const uint4 g = __ldcs(reinterpret_cast<const uint4*>(dout + rh * D) + sub);
       const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
       const __nv_bfloat162* pg = reinterpret_cast<const __nv_bfloat162*>(&g);
 #pragma unroll
       for (int k = 0; k < 4; ++k)
         acc += __low2float(pa[k]) * __low2float(pg[k]) + __high2float(pa[k]) * __high2float(pg[k]);
     }
-    const int bb = int(row / S), s = int(row % S);
-    delta[((long long)bb * nh + h) * S + s] = acc;
+#pragma unroll
+    for (int w = G / 2; w > 0; w >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, w);
+    if (sub == 0 && idx < n) {
+      const int h = int(rh % nh);
+      const long long row = rh / nh;  // b*S + s
+      const int bb = int(row / S), s = int(row % S);
+      delta[((long long)bb * nh + h) * S + s] = acc;
+    }
   }
 }
 
@@ -1921,7 +1928,8 @@ cudaError_t launch_bwd(const AttnBwdDesc& a, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(a.dq_acc, 0, size_t(M) * a.nh * D * sizeof(float), s);
     if (e != cudaSuccess) return e;
   }
-  attn_delta_kernel<D><<<ew_blocks(M * a.nh), 256, 0, s>>>(a.out, a.dout, a.delta, a.S, a.nh, a.mb);
+  attn_delta_kernel<D><<<ew_blocks(M * a.nh * (D / 8)), 256, 0, s>>>(a.out, a.dout, a.delta, a.S,
+                                                                      a.nh, a.mb);
   BwdParams p;
   p.dq_acc = a.dq_acc;
   p.lse = a.lse;
