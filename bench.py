@@ -544,10 +544,16 @@ def main():
                       "frac_of_share_peak": (fl / (ms / 1e3) / 1e12 / (pk["bf16_tflops_sustained"] * sh))
                       if ms > 0 and sh > 0 else None}
                      for i, (fl, ms, nl_, sh) in enumerate(r["lin_per_rank"])]
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "gemm_traffic.json")
-    if os.path.exists(tf):
-        traffic = json.load(open(tf)).get("bytes_per_launch")
+    # DRAM bytes per TP-GEMM launch (read + write) from one ncu --set full
+    # capture of the step's twelve linear GEMM shapes (scripts/gemm_traffic_probe.py,
+    # launch-weighted like `achieved`), beside their algorithmic bytes
+    traffic, traffic_alg = None, None
+    for tf in (os.path.join(ROOT, "profiles", "r02_gemm_traffic.json"),
+               os.path.join(ROOT, "profiles", "gemm_traffic.json")):
+        if os.path.exists(tf):
+            tj = json.load(open(tf))
+            traffic, traffic_alg = tj.get("bytes_per_launch"), tj.get("algorithmic_bytes_per_launch")
+            break
     cpu = None
     if a.gpus == 1 and not a.no_cpu_baseline:
         cb = cpu_reference(asym, steps=1, warmup=0)
@@ -590,7 +596,8 @@ def main():
                      "launches_per_step": (n0 * r["n_mb"][0]) if r.get("gemm_graph") else n0 / max(
                          r["stats"].get("gemm_profile", {}).get("steps", 1), 1),
                      "algorithmic_flops_per_launch": lin_flops_launch,
-                     "avg_launch_ms": lin_ms_launch, "traffic": traffic},
+                     "avg_launch_ms": lin_ms_launch, "traffic": traffic,
+                     "traffic_algorithmic_bytes": traffic_alg},
         "gemm_profile_rank0": r.get("gemm_graph") or r["stats"].get("gemm_profile"),
         "phase_ms_rank0": r["stats"].get("ms"),
         "timeline_ms_rank0_profiled": r["stats"].get("timeline_ms"),
