@@ -358,6 +358,14 @@ class Executor {
       qkvw = 3 * d * nh;
       kr = d * nh;
     }
+    // the fused tcgen05 attention kernels cover d = 64 / 128; the plan admits
+    // d up to 256 (multiples of 64): those models run the unfused GEMM +
+    // softmax attention on the GPU instead of failing at the first step
+    if (cfg.attention == "fused" && d != 64 && d != 128) {
+      cfg.attention = "unfused";
+      attention_note_ = "unfused (fused kernels cover head_dim 64 / 128; head_dim " +
+                        std::to_string(d) + ")";
+    }
     if (cfg.validate_only) {
       // host-only dry run: size the per-rank arena (no device needed)
       if (role.active) allocate();
@@ -1028,6 +1036,7 @@ class Executor {
     }
   }
   bool pad_ = false;
+  std::string attention_note_;
 
   // ------------------------------------------------------------ forward
   LayerActs& acts(Slot& sl, int64_t l) { return cfg.recompute ? rc_acts_ : sl.layers[size_t(l)]; }
@@ -1869,6 +1878,7 @@ class Executor {
     j["sm_total"] = sm_total;
     j["sm_applied"] = sm_applied;
     j["sm_cap_mode"] = sm_mode;
+    j["attention"] = attention_note_.empty() ? cfg.attention : attention_note_;
     j["wgrad_group"] = wg_;
     j["wgrad_group_buffers"] = wg_nbuf_;
     j["tp_reduce"] = tp_peer_ ? (tp_crit_ >= 0 ? "peer(pull from tp rank " + std::to_string(tp_crit_) + ")" : std::string("peer(push)")) : (role.tp > 1 ? std::string("nccl") : std::string("none"));

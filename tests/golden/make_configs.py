@@ -91,6 +91,10 @@ MODELS = {
     "llama30b_2l_s256": {"num_layers": 2, "hidden_dim": 6656, "seq_len": 256,
                          "bytes_per_element": 2, "num_heads": 52, "ffn_dim": 17920,
                          "vocab_size": 1024},
+    # head_dim 256 (beyond the fused attention kernels' 64 / 128): the executor
+    # runs the unfused GEMM + softmax attention
+    "tiny_d256": {"num_layers": 2, "hidden_dim": 512, "seq_len": 128, "bytes_per_element": 4,
+                  "num_heads": 2, "ffn_dim": 1024, "vocab_size": 512},
     # the benchmarked 7B shape (H 4096, 32 heads, F 11008, V 32000, S 2048) cut
     # to 2 layers: GPU-vs-oracle parity of the headline workload's kernels
     "llama7b_2l": {"num_layers": 2, "hidden_dim": 4096, "seq_len": 2048, "bytes_per_element": 2,
@@ -142,6 +146,7 @@ HAND = {
     # its TP communicator's rank 0 (lowest world rank) is not the stage leader
     "tiny_pp3_4_perm": ("b200_4_tiers", "tiny", plan([pipe(8, 2, [
         stage(["g0"], 0, 2), stage(["g3", "g2"], 2, 1, [3, 1]), stage(["g1"], 3, 1)])], 4)),
+    "tiny_d256_1": ("b200_1", "tiny_d256", plan([pipe(4, 2, [stage(["g0"], 0, 2)])], 2)),
     # one micro-batch of 160 x 128 = 20480 tokens (> 16384: the embedding
     # backward sorts 64-bit keys with the device radix sort)
     "tiny_bigmb": ("b200_1", "tiny", plan([pipe(160, 160, [stage(["g0"], 0, 4)])], 4)),

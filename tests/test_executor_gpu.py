@@ -212,3 +212,13 @@ def test_large_micro_batch(tmp_path):
     """A micro-batch of 20480 tokens (above the one-CTA sort of the embedding
     backward): the 64-bit-key radix-sort path, against the oracle."""
     check_against_oracle("tiny_bigmb", run_plan("tiny_bigmb", tmp_path, steps=1))
+
+
+def test_head_dim_256_falls_back_to_unfused_attention(tmp_path):
+    """head_dim 256 (the plan admits multiples of 64 up to 256; the fused
+    kernels cover 64 / 128): the step runs the unfused tcgen05 GEMM + softmax
+    attention, reports it, and matches the oracle."""
+    ranks = run_plan("tiny_d256_1", tmp_path, steps=1)
+    check_against_oracle("tiny_d256_1", ranks)
+    st = json.loads(bytes(ranks[0]["stats"]).decode())
+    assert st["attention"].startswith("unfused"), st["attention"]
