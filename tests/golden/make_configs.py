@@ -181,6 +181,10 @@ HAND = {
     # split 2/1/1 and an uneven TP stage (3:1 over a full and a half-capped B200)
     "llama13b_4l_pp3": ("b200_4_tiers", "llama13b_4l_s256", plan([pipe(4, 1, [
         stage(["g0"], 0, 2), stage(["g1", "g2"], 2, 1, [3, 1]), stage(["g3"], 3, 1)])], 4)),
+    # cfg4's uneven TP=3 stage (widths 2:2:1, as llama13b_pp3_asymtp) at 13B
+    # layer shapes: TP 3 over [F, F, 1/2] for layers 0-2, then one 1/2 B200
+    "llama13b_4l_tp3": ("b200_4_tiers", "llama13b_4l_s256", plan([pipe(4, 1, [
+        stage(["g0", "g1", "g2"], 0, 3, [2, 2, 1]), stage(["g3"], 3, 1)])], 4)),
     # mixed TP + PP + DP at 13B layer shapes: pipeline 0 = TP 2:1 stage (3 layers)
     # + 1-layer stage, 3 samples; pipeline 1 = one B200, 2 samples
     "llama13b_4l_mixed": ("b200_4_tiers", "llama13b_4l_s256", plan([

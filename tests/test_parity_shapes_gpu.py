@@ -129,10 +129,11 @@ def test_large_layer_shapes_tp31(tmp_path, name):
     _check(name, run_plan(name, tmp_path, timeout=1200))
 
 
-@pytest.mark.parametrize("name", ["llama13b_4l_pp3", "llama13b_4l_mixed"])
+@pytest.mark.parametrize("name", ["llama13b_4l_pp3", "llama13b_4l_mixed", "llama13b_4l_tp3"])
 def test_13b_four_gpu_plans(tmp_path, name):
-    """cfg4 analogue (3-stage PP, uneven split, uneven TP stage) and mixed
-    TP + PP + DP with mismatched TP degrees, at 13B layer shapes."""
+    """cfg4 analogues at 13B layer shapes: 3-stage PP (uneven split, uneven
+    TP stage); mixed TP + PP + DP with mismatched TP degrees; cfg4's uneven
+    TP = 3 stage (widths 2:2:1 -> heads 16/16/8, two peers per exchange)."""
     if ngpu() < world_of(name):
         pytest.skip("needs 4 GPUs")
     ranks = run_plan(name, tmp_path, timeout=1200)
