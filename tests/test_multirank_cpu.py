@@ -28,7 +28,7 @@ def _port():
 
 @pytest.mark.parametrize("world,plans", [
     (2, "tiny_tp31,tiny_dp53,tiny_pp31,llama7b_4l_tp31,llama7b_2l_tp31,llama13b_2l_tp31"),
-    (4, "tiny_mixed4,tiny_pp3_4,tiny_pp3_4_perm,llama13b_4l_pp3,llama13b_4l_mixed,"
+    (4, "tiny_mixed4,tiny_pp3_4,tiny_pp3_4_perm,llama13b_4l_pp3,llama13b_4l_mixed,llama13b_4l_tp3,"
         "llama7b_4l_4_cal,llama7b_4l_4_even"),
 ])
 def test_multirank_host_path_gloo(world, plans):
