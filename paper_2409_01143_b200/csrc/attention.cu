@@ -589,6 +589,277 @@ __global__ void __launch_bounds__(kThreads2, 1)
   }
 }
 
+// P = exp2(s * scale_log2 - m) packed in place as bf16 pairs: sv[k] holds
+// columns (2k, 2k + 1) for k < T / 2 (the TMEM A-operand layout of P);
+// returns the row sum of the fp32 values
+template <bool DIAG>
+HX_DEVICE float exp_pack_p(uint32_t (&sv)[T], int r, float scale_log2, float m) {
+  float lsp[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) lsp[k] = 0.f;
+#pragma unroll
+  for (int k = 0; k < T / 2; ++k) {
+    const int i = 2 * k;
+    float e0 = ex2(fmaf(__uint_as_float(sv[i]), scale_log2, -m));
+    float e1 = ex2(fmaf(__uint_as_float(sv[i + 1]), scale_log2, -m));
+    e0 = (!DIAG || i <= r) ? e0 : 0.f;
+    e1 = (!DIAG || i + 1 <= r) ? e1 : 0.f;
+    lsp[i % 8] += e0;
+    lsp[(i + 1) % 8] += e1;
+    sv[k] = pack_bf16x2(e0, e1);
+  }
+  return ((lsp[0] + lsp[1]) + (lsp[2] + lsp[3])) + ((lsp[4] + lsp[5]) + (lsp[6] + lsp[7]));
+}
+
+// ------------------------------------------------------------------ forward, v3
+// attn_fwd3_kernel with P kept in tensor memory: each softmax thread writes
+// its row's P (bf16 pairs) over the S columns it has just read (tcgen05.st),
+// and O += P V reads its A operand from TMEM -- P no longer goes through
+// shared memory; the freed 64 KB double-buffer V.  S_g(j+1) overwrites those
+// columns, so the MMA issuer waits for PV_g(j) (o_full) before issuing it.
+
+template <int D>
+struct Fwd3Cfg {
+  static constexpr uint32_t TILE = T * D * 2;
+  static constexpr uint32_t SMEM = 1024 + 2 * TILE /*Q*/ + 2 * TILE /*K*/ + 2 * TILE /*V*/ + 256;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads2, 1)
+    attn_fwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
+  using C = Fwd3Cfg<D>;
+  constexpr int DA = D / 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                  // [2 tiles]
+  uint8_t* sK = sQ + 2 * C::TILE;      // [2 slots]
+  uint8_t* sV = sK + 2 * C::TILE;      // [2 slots]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + 2 * C::TILE);
+  uint64_t* q_full = bar;        // Q_A + Q_B
+  uint64_t* k_full = bar + 1;    // [2]
+  uint64_t* k_empty = bar + 3;   // [2]
+  uint64_t* v_full = bar + 5;    // [2]
+  uint64_t* v_empty = bar + 15;  // [2]
+  uint64_t* s_full = bar + 7;    // [2 tiles]
+  uint64_t* s_empty = bar + 9;   // [2 tiles]
+  uint64_t* p_full = bar + 11;   // [2 tiles]
+  uint64_t* o_full = bar + 13;   // [2 tiles]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 18);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int nqt = p.S / T;
+  const int npairs = (nqt + 1) / 2;
+  // heaviest pairs of every head first (longest-first over the grid)
+  const int nz = p.mb * p.nh;
+  const int pr = npairs - 1 - int(blockIdx.x / nz);
+  const int zh = int(blockIdx.x % nz);
+  const int h = zh % p.nh;
+  const int b = zh / p.nh;
+  const int qa = 2 * pr;                 // query tile of warpgroup A
+  const bool has_b = qa + 1 < nqt;       // query tile qa+1 of warpgroup B
+  const int nt_a = qa + 1;               // key tiles visited by A / B
+  const int nt_b = has_b ? qa + 2 : 0;
+  const int nkv = has_b ? nt_b : nt_a;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&o_full[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+    if (warp == 0 && lane == 0) {
+      mbar_arrive_expect_tx(q_full, (has_b ? 2 : 1) * C::TILE);
+      for (int a = 0; a < DA; ++a) {
+        tma_load_4d(sQ + a * ATOM, &tmQ, q_full, a * 64, qa * T, h, b);
+        if (has_b) tma_load_4d(sQ + C::TILE + a * ATOM, &tmQ, q_full, a * 64, (qa + 1) * T, h, b);
+      }
+      for (int j = 0; j < nkv; ++j) {
+        const int slot = j & 1;
+        mbar_wait(&k_empty[slot], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&k_full[slot], C::TILE);
+        for (int a = 0; a < DA; ++a)
+          tma_load_4d(sK + slot * C::TILE + a * ATOM, &tmK, &k_full[slot], a * 64, j * T, h, b);
+        mbar_wait(&v_empty[slot], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&v_full[slot], C::TILE);
+        for (int kb = 0; kb < 2; ++kb)
+          for (int a = 0; a < DA; ++a)
+            tma_load_4d(sV + slot * C::TILE + kb * (DA * 8192) + a * 8192, &tmV, &v_full[slot],
+                        a * 64, j * T + kb * 64, h, b);
+      }
+    } else if (warp == 1 && lane == 0) {
+      const uint32_t id_s = idesc_bf16(T, T, 0, 0);
+      const uint32_t id_o = idesc_bf16(T, D, 0, 1);
+      mbar_wait(q_full, 0);
+      auto issue_s = [&](int g, int j) {  // S_g(j) = Q_g K_j^T
+        const int slot = j & 1;
+        mbar_wait(&k_full[slot], (j >> 1) & 1);
+        mbar_wait(&s_empty[g], (j & 1) ^ 1);
+        // the S_g columns hold P_g(j-1) until PV_g(j-1) has read it
+        if (j > 0) mbar_wait(&o_full[g], (j - 1) & 1);
+        tc_fence_after();
+        const uint32_t q_addr = smem_u32(sQ + g * C::TILE);
+        const uint32_t k_addr = smem_u32(sK + slot * C::TILE);
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks)
+          tc_mma_f16(tbase + uint32_t(g * T), kdesc(q_addr, ks), kdesc(k_addr, ks), id_s,
+                     ks > 0 ? 1u : 0u);
+        tc_commit(&s_full[g]);
+      };
+      auto issue_o = [&](int g, int j) {  // O_g += P_g(j) V_j, P_g(j) from TMEM
+        mbar_wait(&p_full[g], j & 1);
+        tc_fence_after();
+        const uint32_t v_addr = smem_u32(sV + (j & 1) * C::TILE);
+#pragma unroll
+        for (int ks = 0; ks < T / 16; ++ks)
+          tc_mma_f16_ts(tbase + uint32_t(2 * T + g * T), tbase + uint32_t(g * T + ks * 8),
+                        mndesc<DA>(v_addr, ks), id_o, (j > 0 || ks > 0) ? 1u : 0u);
+        tc_commit(&o_full[g]);
+      };
+      // S_g(j+1) is issued as soon as warpgroup g has read S_g(j) out of TMEM,
+      // so it computes during the softmax of tile j and both warpgroups'
+      // softmax run concurrently (latency hiding across the pair)
+      if (nt_a > 0) issue_s(0, 0);
+      if (has_b) issue_s(1, 0);
+      for (int j = 0; j < nkv; ++j) {
+        const bool a_on = j < nt_a, b_on = j < nt_b;
+        mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+        if (a_on) {
+          issue_o(0, j);
+          if (j + 1 < nt_a) issue_s(0, j + 1);
+        }
+        if (b_on) {
+          issue_o(1, j);
+          if (j + 1 < nt_b) issue_s(1, j + 1);
+        }
+        tc_commit(&v_empty[j & 1]);       // V_j consumed once both PV products finish
+        tc_commit(&k_empty[j & 1]);       // K_j consumed by both S products
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
+    const int g = (warp - 4) / 4;  // 0 = A, 1 = B
+    const int ew = (warp - 4) % 4;
+    const int qt = qa + g;
+    const int ntiles = g == 0 ? nt_a : nt_b;
+    if (ntiles > 0) {
+      const int r = ew * 32 + lane;
+      const uint32_t lane_off = uint32_t(ew * 32) << 16;
+      const uint32_t s_col = uint32_t(g * T), o_col = uint32_t(2 * T + g * T);
+      constexpr float kSlack = 8.f;
+      float m = -FLT_MAX, l = 0.f;
+      for (int j = 0; j < ntiles; ++j) {
+        const bool diag = j == qt;
+        mbar_wait(&s_full[g], j & 1);
+        tc_fence_after();
+        uint32_t sv[T];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t* v = sv + c * 32;
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+              "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+                "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]),
+                "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+                "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+                "=r"(v[30]), "=r"(v[31])
+              : "r"(tbase + lane_off + s_col + uint32_t(c * 32)));
+        }
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[g]);
+        float mt = (diag ? row_max<true>(sv, r) : row_max<false>(sv, r)) * p.scale_log2;
+        if (j > 0) {  // PV_{j-1} done: P buffer free and O stable
+          mbar_wait(&o_full[g], (j - 1) & 1);
+          tc_fence_after();
+        }
+        if (__any_sync(0xffffffffu, mt > m + kSlack)) {
+          const float m_new = fmaxf(m, mt);
+          const float alpha = ex2(m - m_new);
+          if (j > 0) {
+#pragma unroll 1
+            for (int c = 0; c < D / 32; ++c) {
+              uint32_t v[32];
+              tmem_ld_32x32b_x32(tbase + lane_off + o_col + uint32_t(c * 32), v);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+              tmem_st_32x32b_x32(tbase + lane_off + o_col + uint32_t(c * 32), v);
+            }
+            tmem_st_wait();
+          }
+          l *= alpha;
+          m = m_new;
+        }
+        l += diag ? exp_pack_p<true>(sv, r, p.scale_log2, m)
+                  : exp_pack_p<false>(sv, r, p.scale_log2, m);
+        // P (bf16 pairs, K-major) over this row's S columns [0, 64)
+        tmem_st_32x32b_x32(tbase + lane_off + s_col, *reinterpret_cast<const uint32_t(*)[32]>(sv));
+        tmem_st_32x32b_x32(tbase + lane_off + s_col + 32u,
+                           *reinterpret_cast<const uint32_t(*)[32]>(sv + 32));
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[g]);
+      }
+      mbar_wait(&o_full[g], (ntiles - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / l;
+      const int qi = qt * T + r;
+      __nv_bfloat16* dst = p.out + ((long long)b * p.S + qi) * p.ldo + (long long)h * D;
+#pragma unroll 1
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tbase + lane_off + o_col + uint32_t(c * 32), v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 w;
+          w.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]) * inv, __uint_as_float(v[8 * q + 1]) * inv);
+          w.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv);
+          w.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv);
+          w.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv);
+          reinterpret_cast<uint4*>(dst)[c * 4 + q] = w;
+        }
+      }
+      p.lse[((long long)b * p.nh + h) * p.S + qi] = m + log2f(l);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
 // ------------------------------------------------------------------ backward
 // CTA = one (sample, head, 128-key tile kt); loops over query tiles i >= kt.
 // Transposed formulation so TMEM rows are keys:
@@ -1868,6 +2139,9 @@ cudaError_t launch_fwd(const AttnDesc& a, cudaStream_t s) {
     e = cudaFuncSetAttribute(attn_fwd2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(C2::SMEM));
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(attn_fwd3_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(Fwd3Cfg<D>::SMEM));
+    if (e != cudaSuccess) return e;
     attr = true;
   }
   const long long W = 3LL * a.nh * D;
@@ -1884,7 +2158,10 @@ cudaError_t launch_fwd(const AttnDesc& a, cudaStream_t s) {
   p.mb = a.mb;
   p.ldo = a.nh * D;
   p.scale_log2 = a.scale * 1.4426950408889634f;
-  if (g_fwd_variant == 2) {
+  if (g_fwd_variant == 3) {
+    const int grid = ((a.S / T + 1) / 2) * a.nh * a.mb;
+    attn_fwd3_kernel<D><<<grid, kThreads2, Fwd3Cfg<D>::SMEM, s>>>(q, k, v, p);
+  } else if (g_fwd_variant == 2) {
     const int grid = ((a.S / T + 1) / 2) * a.nh * a.mb;
     attn_fwd2_kernel<D><<<grid, kThreads2, C2::SMEM, s>>>(q, k, v, p);
   } else {
@@ -1957,7 +2234,7 @@ cudaError_t launch_bwd(const AttnBwdDesc& a, cudaStream_t s) {
 
 }  // namespace
 
-void attention_fwd_variant(int v) { g_fwd_variant = v == 1 ? 1 : 2; }
+void attention_fwd_variant(int v) { g_fwd_variant = (v >= 1 && v <= 3) ? v : 2; }
 void attention_bwd_variant(int v) { g_bwd_variant = (v >= 1 && v <= 3) ? v : 3; }
 
 cudaError_t attention_fwd(const AttnDesc& a, cudaStream_t s) {

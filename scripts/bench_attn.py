@@ -9,8 +9,8 @@ sys.path.insert(0, __file__.rsplit("/scripts/", 1)[0])
 from paper_2409_01143_b200 import _lib as L  # noqa: E402
 
 
-def main(mb=1, S=2048, nh=32, d=128, iters=10, variant=3):
-    L.hexexec_k_attn_variant(0, variant)
+def main(mb=1, S=2048, nh=32, d=128, iters=10, variant=3, fwd_variant=2):
+    L.hexexec_k_attn_variant(fwd_variant, variant)
     torch.manual_seed(0)
     qkv = torch.randn(mb * S, nh * 3 * d, device="cuda").bfloat16()
     out = torch.zeros(mb * S, nh * d, device="cuda", dtype=torch.bfloat16)
@@ -72,9 +72,12 @@ def main(mb=1, S=2048, nh=32, d=128, iters=10, variant=3):
                               "bwd_ms": round(tb, 4), "bwd_tflops": round(2.5 * flops / tb / 1e9, 1)}
     except Exception as ex:  # noqa: BLE001
         res["flash_attn2"] = {"error": str(ex)[:200]}
-    print(json.dumps({"shape": [mb, S, nh, d], "bwd_variant": variant, **res}))
+    print(json.dumps({"shape": [mb, S, nh, d], "fwd_variant": fwd_variant, "bwd_variant": variant,
+                      **res}))
 
 
 if __name__ == "__main__":
-    for v in (int(a) for a in (sys.argv[1:] or ["3", "2", "1"])):
-        main(variant=v)
+    # arguments: [fwd:]bwd variant pairs, e.g. 3:3 2:3 2:1
+    for a in (sys.argv[1:] or ["3", "2", "1"]):
+        f, _, b = a.rpartition(":")
+        main(variant=int(b), fwd_variant=int(f) if f else 2)

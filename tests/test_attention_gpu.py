@@ -29,9 +29,13 @@ def _ref(qkv, mb, S, nh, d, scale):
     return o.transpose(1, 2).reshape(mb * S, nh * d), lse.reshape(mb * nh, S), (q, k, v)
 
 
-@pytest.mark.parametrize("mb,S,nh,d", [(1, 256, 2, 128), (2, 384, 3, 64), (1, 2048, 2, 128)])
-def test_attention_forward(cuda, mb, S, nh, d):
+@pytest.mark.parametrize("variant", [3, 2])
+@pytest.mark.parametrize("mb,S,nh,d", [(1, 256, 2, 128), (2, 384, 3, 64), (1, 2048, 2, 128),
+                                       (1, 2048, 32, 128), (1, 128, 1, 64)])
+def test_attention_forward(cuda, mb, S, nh, d, variant):
+    """v3 (P in TMEM, V double-buffered) and v2 forward kernels."""
     L = _L()
+    assert L.hexexec_k_attn_variant(variant, 0) == 0
     torch.manual_seed(0)
     qkv = torch.randn(mb * S, nh * 3 * d, device=cuda).bfloat16()
     out = torch.zeros(mb * S, nh * d, device=cuda, dtype=torch.bfloat16)
@@ -40,6 +44,7 @@ def test_attention_forward(cuda, mb, S, nh, d):
     assert L.hexexec_k_attn_fwd(qkv.data_ptr(), out.data_ptr(), lse.data_ptr(), S, nh, d, mb,
                                 scale, None) == 0
     torch.cuda.synchronize()
+    L.hexexec_k_attn_variant(2, 0)
     ro, rl, _ = _ref(qkv, mb, S, nh, d, scale)
     assert _rel(out, ro) < 1e-2
     assert (lse / math.log2(math.e) - rl).abs().max().item() < 1e-3
@@ -75,3 +80,25 @@ def test_attention_backward(cuda, mb, S, nh, d, variant):
     L.hexexec_k_attn_variant(0, 3)
     for part in range(3):
         assert _rel(g[:, :, part], r[:, :, part]) < 2e-2, part
+
+
+def test_attention_forward_v3_matches_v2_bitwise(cuda):
+    """P kept in TMEM (v3) vs P through shared memory (v2): the same bf16 P,
+    the same MMAs, so the same output and LSE bit for bit (also a check that
+    the next S product never overwrites P before O += P V has read it)."""
+    L = _L()
+    torch.manual_seed(3)
+    mb, S, nh, d = 2, 2048, 8, 128
+    qkv = torch.randn(mb * S, nh * 3 * d, device=cuda).bfloat16()
+    outs = []
+    for v in (2, 3, 3, 3):
+        out = torch.zeros(mb * S, nh * d, device=cuda, dtype=torch.bfloat16)
+        lse = torch.zeros(mb * nh, S, device=cuda)
+        assert L.hexexec_k_attn_variant(v, 0) == 0
+        assert L.hexexec_k_attn_fwd(qkv.data_ptr(), out.data_ptr(), lse.data_ptr(), S, nh, d, mb,
+                                    1.0 / math.sqrt(d), None) == 0
+        torch.cuda.synchronize()
+        outs.append((out, lse))
+    L.hexexec_k_attn_variant(2, 0)
+    for o, l in outs[1:]:
+        assert torch.equal(o, outs[0][0]) and torch.equal(l, outs[0][1])
