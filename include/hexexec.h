@@ -188,7 +188,8 @@ hexexec_status hexexec_k_gemm_tile_auto(int on);
  * dq/dk/dv into dqkv [mb*S, nh*3*d] (delta / dq_acc: fp32 scratch of
  * mb*nh*S and mb*S*nh*d floats). */
 /* kernel variants of later attention calls (process-wide; 0 = unchanged):
- * fwd 2 = two query tiles per CTA (default), 1 = one; bwd 3 = P^T kept in
+ * fwd 3 = two query tiles per CTA with P kept in TMEM (default), 2 = the
+ * same with P through shared memory, 1 = one tile per CTA; bwd 3 = P^T kept in
  * TMEM + separate dQ epilogue warpgroup (default), 2 = dQ epilogue warpgroup
  * with P^T through shared memory, 1 = softmax warps stream dQ (r01) */
 hexexec_status hexexec_k_attn_variant(int fwd, int bwd);

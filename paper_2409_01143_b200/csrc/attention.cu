@@ -2086,7 +2086,9 @@ __global__ void attn_dq_cast_rope_kernel(float* __restrict__ dq, __nv_bfloat16* 
 }
 
 // ------------------------------------------------------------------ host
-int g_fwd_variant = 2;  // 2 = two query tiles per CTA (ping-pong), 1 = one tile
+// 3 = two query tiles per CTA with P in TMEM (default), 2 = the same with P
+// through shared memory, 1 = one tile per CTA
+int g_fwd_variant = 3;
 // 3 = P^T in TMEM + dQ epilogue warpgroup, 2 = dQ epilogue warpgroup,
 // 1 = softmax warps stream dQ (r01)
 int g_bwd_variant = 3;
@@ -2234,7 +2236,7 @@ cudaError_t launch_bwd(const AttnBwdDesc& a, cudaStream_t s) {
 
 }  // namespace
 
-void attention_fwd_variant(int v) { g_fwd_variant = (v >= 1 && v <= 3) ? v : 2; }
+void attention_fwd_variant(int v) { g_fwd_variant = (v >= 1 && v <= 3) ? v : 3; }
 void attention_bwd_variant(int v) { g_bwd_variant = (v >= 1 && v <= 3) ? v : 3; }
 
 cudaError_t attention_fwd(const AttnDesc& a, cudaStream_t s) {

@@ -20,6 +20,7 @@ struct AttnDesc {
 // forward: out = softmax(scale * q k^T, causal) v ; lse saved for the backward
 cudaError_t attention_fwd(const AttnDesc& a, cudaStream_t s);
 // 2 (default): two query tiles per CTA with ping-pong softmax warpgroups; 1: one tile
+// forward: 3 = P in TMEM (default), 2 = P through shared memory, 1 = one tile / CTA
 void attention_fwd_variant(int v);
 // backward: 3 = P^T in TMEM + dQ epilogue warpgroup (default), 2 = dQ epilogue
 // warpgroup, 1 = the r01 kernel

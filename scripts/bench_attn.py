@@ -9,7 +9,7 @@ sys.path.insert(0, __file__.rsplit("/scripts/", 1)[0])
 from paper_2409_01143_b200 import _lib as L  # noqa: E402
 
 
-def main(mb=1, S=2048, nh=32, d=128, iters=10, variant=3, fwd_variant=2):
+def main(mb=1, S=2048, nh=32, d=128, iters=10, variant=3, fwd_variant=3):
     L.hexexec_k_attn_variant(fwd_variant, variant)
     torch.manual_seed(0)
     qkv = torch.randn(mb * S, nh * 3 * d, device="cuda").bfloat16()
@@ -80,4 +80,4 @@ if __name__ == "__main__":
     # arguments: [fwd:]bwd variant pairs, e.g. 3:3 2:3 2:1
     for a in (sys.argv[1:] or ["3", "2", "1"]):
         f, _, b = a.rpartition(":")
-        main(variant=int(b), fwd_variant=int(f) if f else 2)
+        main(variant=int(b), fwd_variant=int(f) if f else 3)

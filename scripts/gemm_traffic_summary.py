@@ -33,8 +33,10 @@ def main():
              "ms": 1e3, "usecond": 1.0, "nsecond": 1e-3}
     out = []
     for sh, r in zip(shapes, data):
-        d = {h: (float(v.replace(",", "")) * scale.get(u, 1.0) if v.replace(".", "").replace(",", "").isdigit() else v)
-             for h, u, v in zip(hdr, units, r)}
+        d = {}
+        for h, u, v in zip(hdr, units, r):
+            if h.startswith(("dram__", "gpu__", "sm__")):
+                d[h] = float(v.replace(",", "")) * scale.get(u, 1.0)
         traffic = d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"]
         out.append(dict(sh, duration_us=round(d["gpu__time_duration.sum"], 2),
                         dram_bytes=traffic, traffic_over_algorithmic=round(traffic / sh["algorithmic_bytes"], 3),

@@ -44,7 +44,7 @@ def test_attention_forward(cuda, mb, S, nh, d, variant):
     assert L.hexexec_k_attn_fwd(qkv.data_ptr(), out.data_ptr(), lse.data_ptr(), S, nh, d, mb,
                                 scale, None) == 0
     torch.cuda.synchronize()
-    L.hexexec_k_attn_variant(2, 0)
+    L.hexexec_k_attn_variant(3, 0)
     ro, rl, _ = _ref(qkv, mb, S, nh, d, scale)
     assert _rel(out, ro) < 1e-2
     assert (lse / math.log2(math.e) - rl).abs().max().item() < 1e-3
@@ -99,6 +99,6 @@ def test_attention_forward_v3_matches_v2_bitwise(cuda):
                                     1.0 / math.sqrt(d), None) == 0
         torch.cuda.synchronize()
         outs.append((out, lse))
-    L.hexexec_k_attn_variant(2, 0)
+    L.hexexec_k_attn_variant(3, 0)
     for o, l in outs[1:]:
         assert torch.equal(o, outs[0][0]) and torch.equal(l, outs[0][1])
