@@ -1946,11 +1946,13 @@ __global__ void __launch_bounds__(kBwd3Threads, 1)
 }
 
 // delta[z][q] = sum_e dO[q, e] * O[q, e]: D/8 consecutive threads per (row,
-// head), 16-byte coalesced loads of O and dO, shuffle reduction
+// head), 16-byte coalesced loads of O and dO, shuffle reduction; the same
+// pass zeroes the fp32 dq accumulator (same [M, nh*D] layout) for the
+// backward's TMA reduce-adds (no separate memset)
 template <int D>
 __global__ void attn_delta_kernel(const __nv_bfloat16* __restrict__ o,
-                                  const __nv_bfloat16* __restrict__ dout, float* delta, int S,
-                                  int nh, int mb) {
+                                  const __nv_bfloat16* __restrict__ dout, float* delta,
+                                  float* __restrict__ dq_zero, int S, int nh, int mb) {
   constexpr int G = D / 8;  // threads per (row, head): 16 (d 128) or 8 (d 64)
   const long long n = (long long)mb * S * nh * G;
   const int sub = threadIdx.x % G;
@@ -1962,6 +1964,10 @@ __global__ void attn_delta_kernel(const __nv_bfloat16* __restrict__ o,
     if (idx < n) {
       const uint4 a = __ldcs(reinterpret_cast<const uint4*>(o + rh * D) + sub);
       const uint4 g = __ldcs(reinterpret_cast<const uint4*>(dout + rh * D) + sub);
+      // the fp32 dq accumulator has O's layout: zero this thread's 8 elements
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      reinterpret_cast<float4*>(dq_zero + rh * D)[2 * sub] = z;
+      reinterpret_cast<float4*>(dq_zero + rh * D)[2 * sub + 1] = z;
       const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
       const __nv_bfloat162* pg = reinterpret_cast<const __nv_bfloat162*>(&g);
 #pragma unroll
@@ -1981,7 +1987,7 @@ __global__ void attn_delta_kernel(const __nv_bfloat16* __restrict__ o,
 
 // dq (fp32 accumulator [M, nh*D]) -> bf16 q slots of dqkv [M, nh*3*D]
 template <int D>
-__global__ void attn_dq_cast_kernel(float* __restrict__ dq, __nv_bfloat16* __restrict__ dqkv,
+__global__ void attn_dq_cast_kernel(const float* __restrict__ dq, __nv_bfloat16* __restrict__ dqkv,
                                     long long M, int nh) {
   const long long n = M * nh * (D / 8);
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
@@ -1990,10 +1996,8 @@ __global__ void attn_dq_cast_kernel(float* __restrict__ dq, __nv_bfloat16* __res
     const long long t = idx / (D / 8);
     const int h = int(t % nh);
     const long long row = t / nh;
-    float4* src = reinterpret_cast<float4*>(dq + row * nh * D + h * D + c * 8);
+    const float4* src = reinterpret_cast<const float4*>(dq + row * nh * D + h * D + c * 8);
     float4 a = src[0], bq = src[1];
-    src[0] = make_float4(0.f, 0.f, 0.f, 0.f);  // leave the accumulator zero
-    src[1] = make_float4(0.f, 0.f, 0.f, 0.f);
     uint4 w;
     w.x = pack_bf16x2(a.x, a.y);
     w.y = pack_bf16x2(a.z, a.w);
@@ -2024,7 +2028,7 @@ __device__ __forceinline__ uint4 f32x8_to_bf16(const float* f) {
   return w;
 }
 template <int D>
-__global__ void attn_dq_cast_rope_kernel(float* __restrict__ dq, __nv_bfloat16* __restrict__ dqkv,
+__global__ void attn_dq_cast_rope_kernel(const float* __restrict__ dq, __nv_bfloat16* __restrict__ dqkv,
                                          const float2* __restrict__ tab, long long M, int S, int nh) {
   constexpr int half = D / 2, g8 = half / 8;
   const long long n = M * nh * g8;
@@ -2044,7 +2048,7 @@ __global__ void attn_dq_cast_rope_kernel(float* __restrict__ dq, __nv_bfloat16* 
       cs[2 * k + 1] = v.z;
       sn[2 * k + 1] = -v.w;
     }
-    float* src = dq + row * nh * D + h * D + c * 8;
+    const float* src = dq + row * nh * D + h * D + c * 8;
     __nv_bfloat16* qb = dqkv + row * 3LL * nh * D + (long long)h * 3 * D + c * 8;
     __nv_bfloat16* kb = qb + D;
     float qa[8], qh[8], ka[8], kh[8];
@@ -2052,11 +2056,6 @@ __global__ void attn_dq_cast_rope_kernel(float* __restrict__ dq, __nv_bfloat16* 
       const float4 a0 = reinterpret_cast<const float4*>(src)[0], a1 = reinterpret_cast<const float4*>(src)[1];
       const float4 b0 = reinterpret_cast<const float4*>(src + half)[0];
       const float4 b1 = reinterpret_cast<const float4*>(src + half)[1];
-      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);  // leave the accumulator zero
-      reinterpret_cast<float4*>(src)[0] = z;
-      reinterpret_cast<float4*>(src)[1] = z;
-      reinterpret_cast<float4*>(src + half)[0] = z;
-      reinterpret_cast<float4*>(src + half)[1] = z;
       const float fa[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
       const float fb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
@@ -2203,12 +2202,8 @@ cudaError_t launch_bwd(const AttnBwdDesc& a, cudaStream_t s) {
       !encode(&dO, a.dout, D, a.S, a.nh, a.mb, (long long)a.nh * D, D, 64, T) ||
       !encode_f32(&dq, a.dq_acc, (long long)a.nh * D, M))
     return cudaErrorInvalidValue;
-  if (!a.dq_acc_zero) {
-    cudaError_t e = cudaMemsetAsync(a.dq_acc, 0, size_t(M) * a.nh * D * sizeof(float), s);
-    if (e != cudaSuccess) return e;
-  }
-  attn_delta_kernel<D><<<ew_blocks(M * a.nh * (D / 8)), 256, 0, s>>>(a.out, a.dout, a.delta, a.S,
-                                                                      a.nh, a.mb);
+  attn_delta_kernel<D><<<ew_blocks(M * a.nh * (D / 8)), 256, 0, s>>>(a.out, a.dout, a.delta,
+                                                                      a.dq_acc, a.S, a.nh, a.mb);
   BwdParams p;
   p.dq_acc = a.dq_acc;
   p.lse = a.lse;

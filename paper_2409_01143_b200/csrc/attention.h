@@ -32,9 +32,7 @@ struct AttnBwdDesc {
   const __nv_bfloat16* dout = nullptr;  // dO [M, nh*d]
   const float* lse = nullptr;
   float* delta = nullptr;               // [mb*nh, S] scratch: rowsum(dO * O)
-  float* dq_acc = nullptr;              // [M, nh*d] fp32 scratch (zeroed here unless
-                                        // dq_acc_zero; the dq cast leaves it zero)
-  bool dq_acc_zero = false;             // caller guarantees dq_acc is all zero
+  float* dq_acc = nullptr;              // [M, nh*d] fp32 scratch (zeroed by the delta pass)
   __nv_bfloat16* dqkv = nullptr;        // [M, nh*3*d]: dq, dk, dv written in place
   int S = 0, nh = 0, d = 0, mb = 0;
   float scale = 1.f;

@@ -664,7 +664,6 @@ class Executor {
     HX_CUDA(cudaMemsetAsync(sp_, 0, sizeof(StepParams), stream));
     HX_CUDA(cudaMemsetAsync(gemm_ws_, 0, kGemmWsBytes, stream));
     HX_CUDA(cudaMemsetAsync(gemm_cnt_, 0, kGemmWsCounters * sizeof(int), stream));
-    HX_CUDA(cudaMemsetAsync(dq_acc_, 0, size_t(M * kr) * 4, stream));
     tokens = arena.take<int32_t>(role.batch * (S + 1));
     HX_CUDA(cudaMallocHost(&tokens_pinned, size_t(role.batch * (S + 1)) * 4));
     HX_CUDA(cudaMallocHost(&loss_host, 64));
@@ -1307,7 +1306,6 @@ class Executor {
       ad.lse = a.lse;
       ad.delta = delta_;
       ad.dq_acc = dq_acc_;
-      ad.dq_acc_zero = true;  // zeroed at allocation, left zero by every dq cast
       ad.dqkv = dqkv;
       ad.S = int(S);
       ad.nh = int(nh);
