@@ -191,6 +191,7 @@ def gather_sum(vals: list, rank: int, world: int, tag: str) -> list:
 
 
 EXEC_CFG = {}  # --exec-config: extra executor config keys (e.g. {"recompute": true})
+MAX_REF_LAYERS = 4  # layers of the CPU reference's bounded sample (the 4-layer workloads run whole)
 
 
 def log(rank: int, msg: str):
@@ -402,11 +403,16 @@ def cpu_reference(name: str, steps: int, warmup: int) -> dict:
     cl = {"machines": {"box": {"intra_bandwidth_gbps": 900, "intra_latency_us": 3}},
           "devices": [{"id": "cpu", "machine": "box", "memory_gib": 64, "peak_tflops": 1}],
           "inter": {"bandwidth_gbps": 900, "latency_us": 3}}
-    L = md["num_layers"]
+    L_model = md["num_layers"]
+    # deep models (the 32-layer 8-GPU workload): the bounded sample runs the
+    # first MAX_REF_LAYERS layers (identical shapes) and the tokens/s of the
+    # full model is extrapolated by training FLOPs -- labelled in the line
+    L = min(L_model, MAX_REF_LAYERS)
+    md_run = dict(md, num_layers=L)
     plan = {"global_batch": 1, "pipelines": [{"batch": 1, "micro_batch": 1, "stages": [
         {"devices": ["cpu"], "tp": 1, "layer_start": 0, "layer_count": L}]}]}
     t0 = time.perf_counter()
-    st = O.Step(cl, md, json.dumps(plan))
+    st = O.Step(cl, md_run, json.dumps(plan))
     init_s = time.perf_counter() - t0
     stages = st.stage_parts(0)
     S = md["seq_len"]
@@ -449,15 +455,27 @@ def cpu_reference(name: str, steps: int, warmup: int) -> dict:
     except Exception as e:  # noqa: BLE001  (reported, never fatal for the bench)
         planner = {"error": str(e)[:200]}
     t = statistics.mean(times)
-    return {"value": S / t, "unit": "tokens/s", "cores": cores, "kind": "port",
-            "reference_planner": planner, "reference_cost_model": cost,
-            "sample": (f"numpy fp32 oracle (oracle/numeric.py): per step one sample of "
-                       f"{S} tokens through the whole {L}-layer model (embedding, layers, "
-                       f"final norm, LM head, CE; forward + backward), measured, not "
-                       f"extrapolated; AdamW excluded; mean of {steps} after {warmup} "
-                       f"warm-up; BLAS + per-head threads = {cores} host cores"),
-            "sample_ms": [round(x * 1e3, 1) for x in times], "init_s": round(init_s, 1),
-            "ms_per_sample": t * 1e3}
+    factor = 1.0
+    if L < L_model:
+        _, f_run = model_flops(md_run, S)
+        _, f_all = model_flops(md, S)
+        factor = f_run / f_all
+    what = (f"the whole {L}-layer model" if L == L_model else
+            f"embedding + the first {L} of {L_model} layers + final norm, LM head")
+    out = {"value": S / t * factor, "unit": "tokens/s", "cores": cores, "kind": "port",
+           "reference_planner": planner, "reference_cost_model": cost,
+           "sample": (f"numpy fp32 oracle (oracle/numeric.py): per step one sample of "
+                      f"{S} tokens through {what} (CE; forward + backward), measured; "
+                      f"AdamW excluded; mean of {steps} after {warmup} warm-up; BLAS + "
+                      f"per-head threads = {cores} host cores"),
+           "sample_ms": [round(x * 1e3, 1) for x in times], "init_s": round(init_s, 1),
+           "ms_per_sample": t * 1e3}
+    if L < L_model:
+        out["extrapolation"] = {"layers_run": L, "layers": L_model,
+                                "measured_unit_tokens_per_s": S / t,
+                                "training_flop_ratio": factor,
+                                "note": "value = measured unit rate x (unit FLOPs / full-model FLOPs)"}
+    return out
 
 
 def main():
@@ -509,7 +527,8 @@ def main():
                 "dtype": "f32", "data": "synthetic", "config": config,
                 "step_unit": "one sample (seq_len tokens) of the plan's model, fwd + bwd",
                 "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample",
-                                                     "reference_planner", "sample_ms", "init_s")},
+                                                     "reference_planner", "sample_ms", "init_s",
+                                                     "extrapolation") if k in ref},
                 "e2e": {"value": ref["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0},
                 "reference_cost_model": ref["reference_cost_model"]}
@@ -558,7 +577,7 @@ def main():
     if a.gpus == 1 and not a.no_cpu_baseline:
         cb = cpu_reference(asym, steps=1, warmup=0)
         cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "reference_planner",
-                                  "reference_cost_model")}
+                                  "reference_cost_model", "extrapolation") if k in cb}
     line = {
         "metric": METRIC, "value": s["tokens_per_s"], "unit": "tokens/s", "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": s["ms_per_step"],
