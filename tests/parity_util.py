@@ -94,7 +94,13 @@ def _run_plan(name, tmp_path, steps, xcfg, host_tokens, timeout, read=None, env_
             raise PortInUse()
         sys.stderr.write("\n".join(errs))
     assert all(p.returncode == 0 for p in procs), [p.returncode for p in procs]
-    return [dict(np.load(os.path.join(tmp_path, f"rank{r}.npz"))) for r in range(world)]
+    out = []
+    for r in range(world):
+        f = os.path.join(tmp_path, f"rank{r}.npz")
+        with np.load(f) as z:
+            out.append({k: z[k] for k in z.files})
+        os.remove(f)  # the large-shape plans write several GB per rank
+    return out
 
 
 _ORACLE = {}
