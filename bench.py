@@ -387,6 +387,20 @@ def reference_cost(name: str, seconds: float | None, speeds=None):
 
 
 def cpu_reference(name: str, steps: int, warmup: int) -> dict:
+    """See _cpu_reference.  BLAS threads are set to every host core explicitly:
+    torchrun exports OMP_NUM_THREADS=1 to each rank, which would otherwise pin
+    the numpy BLAS of the N > 1 reference arm to one core."""
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    import numpy  # noqa: F401  (threadpoolctl only sees BLAS libraries already loaded)
+    try:
+        from threadpoolctl import threadpool_limits
+    except ImportError:  # pragma: no cover
+        return _cpu_reference(name, steps, warmup)
+    with threadpool_limits(limits=cores or 1, user_api="blas"):
+        return _cpu_reference(name, steps, warmup)
+
+
+def _cpu_reference(name: str, steps: int, warmup: int) -> dict:
     """The CPU reference of this path: the fp32 numpy oracle port
     (oracle/numeric.py; the reference repo has no numeric training step,
     SURVEY §0) on a bounded sample of the plan's workload, run as is: one
