@@ -72,5 +72,5 @@ def step_grads(st, device="cuda", dtype="bf16"):
         logits = (xf @ P["lm_head"].to(adt).T).float()
         loss = F.cross_entropy(logits, tgt, reduction="sum")
         (loss / count).backward()
-        total += float(loss)
+        total += float(loss.detach())
     return total / count, {k: v.grad.detach().float().cpu().numpy() for k, v in P.items()}
