@@ -200,6 +200,12 @@ HAND = {
     # cfg2 with widths from the calibrated speeds (1270 : 525 ~ 5 : 2)
     "llama7b_4l_tp52": ("b200_2_capped", "llama7b_4l",
                         plan([pipe(8, 1, [stage(["g0", "g1"], 0, 4, [5, 2])])], 4)),
+    # width sweep of cfg2 around the delivered-compute ratio (148 SMs x 1.54 GHz :
+    # 56 SMs x 1.97 GHz ~ 2.1 : 1)
+    "llama7b_4l_tp73": ("b200_2_capped", "llama7b_4l",
+                        plan([pipe(8, 1, [stage(["g0", "g1"], 0, 4, [7, 3])])], 4)),
+    "llama7b_4l_tp21": ("b200_2_capped", "llama7b_4l",
+                        plan([pipe(8, 1, [stage(["g0", "g1"], 0, 4, [2, 1])])], 4)),
     # cfg4: Llama-13B, 3 stages 16/14/10, asymmetric TP inside stages
     "llama13b_pp3_asymtp": ("b200_8_onebox", "llama13b", plan([pipe(16, 1, [
         stage(["g0", "g1", "g4"], 0, 16, [2, 2, 1]),
