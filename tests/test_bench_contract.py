@@ -54,3 +54,32 @@ def test_default_plans_exist():
     for n, names in bench.ALT.items():
         for a in names.split(","):
             assert a in idx
+
+
+def test_cpu_reference_bounded_sample(monkeypatch):
+    """The reference arm's unit: one sample through the whole model when it has
+    at most MAX_REF_LAYERS layers (nothing extrapolated); deeper models run the
+    first MAX_REF_LAYERS layers and label the FLOP-ratio extrapolation.  Only
+    oracle code runs (no product library)."""
+    r = bench.cpu_reference("tiny_1", steps=1, warmup=0)
+    assert r["kind"] == "port" and r["value"] > 0 and "extrapolation" not in r
+    assert r["ms_per_sample"] > 0 and len(r["sample_ms"]) == 1
+    monkeypatch.setattr(bench, "MAX_REF_LAYERS", 2)
+    r2 = bench.cpu_reference("tiny_1", steps=1, warmup=0)
+    ex = r2["extrapolation"]
+    assert ex["layers_run"] == 2 and ex["layers"] == 4 and 0 < ex["training_flop_ratio"] < 1
+    assert abs(r2["value"] - ex["measured_unit_tokens_per_s"] * ex["training_flop_ratio"]) < 1e-6
+
+
+def test_summarize_delivered_clock_mfu():
+    """MFU at delivered clock = reference FLOPs / (sum SMs x median clock x 8192)."""
+    c, m, p, _ = bench.load("llama7b_4l_1gpu")
+    r = {"name": "llama7b_4l_1gpu", "plan": json.loads(p), "model": json.loads(m),
+         "cluster": json.loads(c), "dev_ms": 1000.0, "e2e_ms": 1000.0, "sm_share": 1.0,
+         "loss": 1.0, "clocks": {"sm_mhz_per_gpu": {"0": 1500.0}, "gpu_of_rank": ["0"]},
+         "lin_per_rank": [[0, 0, 0, 1.0]]}
+    s = bench.summarize(r, steps=10, pk={"bf16_tflops": 1646.0})
+    md = bench.full_model(c, m, p)
+    ref, _ = bench.model_flops(md, 8 * 2048)
+    assert abs(s["mfu_at_delivered_clock"] - ref / 0.1 / (148 * 1.5 * 8192e9)) < 1e-9
+    assert abs(s["mfu_ref_convention"] - ref / 0.1 / 1646e12) < 1e-9
