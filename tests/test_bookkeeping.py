@@ -253,3 +253,44 @@ def test_shard_rules():
     r = Plan(c, m, p).layout()["ranks"]
     assert r[0]["heads"] == [0, 24] and r[1]["heads"] == [24, 32]
     assert r[0]["ffn_cols"] == [0, 8256] and r[1]["ffn_cols"] == [8256, 11008]
+
+
+@pytest.mark.parametrize("cfg,ok", [
+    ('{"pp_dtype": "bf16"}', True), ('{"pp_dtype": "fp32"}', True), ('{"pp_dtype": "fp16"}', False),
+    ('{"attention": "unfused", "recompute": true}', True), ('{"tp_reduce": "ring"}', False),
+    ('{"wgrad_group": "x"}', False), ('{"dp_comm_dtype": "fp32", "tp_pull": "sm"}', True),
+])
+def test_exec_config_values(cfg, ok):
+    """Every exec-config key of include/hexexec.h validates its value at the
+    boundary (strict like the reference's config parser, json_io.cpp:263)."""
+    L, _ = product()
+    c, m, p = docs("tiny_1")
+    h = C.c_void_p()
+    err = C.create_string_buffer(256)
+    full = json.dumps(dict(json.loads(cfg), validate_only=True))
+    st = L.hexexec_ctx_create(c.encode(), m.encode(), p.encode(), full.encode(), 0, 1, 0, None, 0,
+                              C.byref(h), err, len(err))
+    if ok:
+        assert st == L.OK, err.value
+        L.hexexec_ctx_free(h)
+    else:
+        assert st == L.ERR_PARSE, (st, err.value)
+
+
+def test_head_dim_256_layout_and_large_micro_batch_sizing():
+    """Host side of the size-limit rows: a head_dim 256 model and a 20480-token
+    micro-batch both size their arena host-only (validate_only), and the
+    head_dim 256 plan reports the unfused attention path."""
+    L, _ = product()
+    for name in ("tiny_d256_1", "tiny_bigmb"):
+        c, m, p = docs(name)
+        h = C.c_void_p()
+        err = C.create_string_buffer(256)
+        st = L.hexexec_ctx_create(c.encode(), m.encode(), p.encode(), b'{"validate_only": true}', 0,
+                                  1, 0, None, 0, C.byref(h), err, len(err))
+        assert st == L.OK, (name, err.value)
+        stats = json.loads(L.take_string(L.hexexec_stats_json(h)))
+        L.hexexec_ctx_free(h)
+        assert stats["arena_bytes"] > 0
+        if name == "tiny_d256_1":
+            assert stats["attention"].startswith("unfused"), stats["attention"]
